@@ -1,0 +1,206 @@
+/*
+ * lanetape_b200.h — C ABI of the B200-native two-pass ∇G engine.
+ *
+ * This is the drop-in boundary for the hot path of arXiv 1901.04200 as the
+ * reference `lanetape` library implements it. Every entry point names the
+ * reference interface it replaces (paths relative to
+ * /root/reference/proj/include/lanetape/):
+ *
+ *   ltg_gradient_of_G   <- lanetape::gradient_of_G(const Tape&, params, targets,
+ *                          const MCConfig&)                 expectation.hpp:346-351
+ *                          (and the Kernel/PathDrawSource overload :300-344)
+ *   ltg_estimate_means  <- lanetape::estimate_means(const Tape&, params,
+ *                          const MCConfig&)                 expectation.hpp:281-286
+ *   ltg_finite_diff_gradient_of_G
+ *                       <- lanetape::finite_diff_gradient_of_G   expectation.hpp:372-400
+ *   ltg_fill_normals    <- lanetape::PhiloxNormalSource::fill    rng.hpp:113-127
+ *   ltg_create_heston   <- lanetape::record_heston_program(ModelSpec) heston.hpp:327-329
+ *                          (the GPU does not interpret tapes: the model description
+ *                          itself is the program)
+ *   ltg_pack_params     <- lanetape::pack_params                 heston.hpp:212-218
+ *
+ * Conventions (mirroring expectation.hpp / tape.hpp error behaviour):
+ *   return LTG_OK (0) on success;
+ *   LTG_EINVAL (1)   where the reference throws std::invalid_argument
+ *                    (size mismatches, paths == 0, bad model, fresh_step2_paths
+ *                    with store mode, ...);
+ *   LTG_ENUMERIC (2) where the reference throws EvalError (a non-finite
+ *                    result — the CLI maps this to exit code 2);
+ *   LTG_ECUDA (3)    CUDA / NCCL runtime failure (no reference analogue);
+ *   ltg_last_error(ctx) returns the message of the last failure on that
+ *   context (ctx == NULL: last failure of a create call on this thread).
+ * All host buffers are caller-owned. A context owns its device memory and
+ * stream; one host thread may use a context at a time (the reference's
+ * gradient_of_G is externally synchronous).
+ *
+ * There is no CPU fallback: every compute entry point runs CUDA kernels and
+ * fails with LTG_ECUDA when no sm_100 device is usable.
+ */
+#ifndef LANETAPE_B200_H
+#define LANETAPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTG_ABI_VERSION 1
+
+#define LTG_OK 0
+#define LTG_EINVAL 1
+#define LTG_ENUMERIC 2
+#define LTG_ECUDA 3
+
+/* Instrument::Kind (heston.hpp:257-263) */
+#define LTG_CALL 0
+#define LTG_PUT 1
+
+/* MemoryMode (expectation.hpp:17) — echoed into the report; the engine picks
+ * its own device memory strategy (HBM checkpoints), see DESIGN.md §4. */
+#define LTG_MODE_RECOMPUTE 0
+#define LTG_MODE_STORE 1
+
+/* arithmetic of the path simulation */
+#define LTG_FP64 0
+#define LTG_FP32 1
+
+typedef struct ltg_ctx ltg_ctx;
+
+/* ModelSpec minus McSettings.paths/seed (heston.hpp:189-283): HestonParams,
+ * LeverageGrid, instruments, steps and dt. kappa..v0 and `leverage` are the
+ * values the program is "recorded" at (pack_params order); the packed
+ * parameter vector x passed to the compute calls overrides them. */
+typedef struct ltg_heston_model {
+    double mu;
+    double s0;
+    double kappa, theta, xi, rho, v0;
+    const double* t_nodes;       /* n_t_nodes, strictly ascending */
+    uint32_t n_t_nodes;
+    const double* s_nodes;       /* n_s_nodes, strictly ascending */
+    uint32_t n_s_nodes;
+    const double* leverage;      /* n_t_nodes * n_s_nodes, t-major */
+    const int32_t* inst_kind;    /* LTG_CALL / LTG_PUT */
+    const double* inst_strike;
+    const uint32_t* inst_maturity_step; /* in [1, steps] */
+    uint32_t n_instruments;
+    uint32_t steps;
+    double dt;
+} ltg_heston_model;
+
+/* Correlated multi-asset log-Euler GBM (BASELINE config 4). Not a model of
+ * the reference's model layer; its oracle is a program recorded with the
+ * reference Tape API (oracle/ref_driver.cpp). Parameters are the n_assets
+ * constant vols. Draw slot of (step k, asset a) is k*n_assets + a. */
+typedef struct ltg_basket_model {
+    uint32_t n_assets;           /* 1..16 */
+    const double* s0;            /* n_assets */
+    double r;                    /* drift constant */
+    const double* chol;          /* n_assets*n_assets, lower-triangular, row-major */
+    const double* sigma;         /* n_assets, recorded-at vols */
+    const uint32_t* inst_asset;
+    const int32_t* inst_kind;
+    const double* inst_strike;
+    const uint32_t* inst_maturity_step;
+    uint32_t n_instruments;
+    uint32_t steps;
+    double dt;
+} ltg_basket_model;
+
+/* MCConfig (expectation.hpp:25-39). lane_width / worker_threads /
+ * store_limit_bytes are CPU execution knobs with no GPU meaning; they are
+ * accepted and ignored, as the reference's results do not depend on them
+ * beyond summation order. */
+typedef struct ltg_mc_config {
+    uint64_t paths;
+    uint64_t seed;
+    int32_t antithetic;
+    int32_t fresh_step2_paths;
+    int32_t memory_mode;         /* LTG_MODE_*, echoed */
+    int32_t precision;           /* LTG_FP64 / LTG_FP32 */
+} ltg_mc_config;
+
+/* GradientReport (expectation.hpp:62-82). Array members are caller-owned
+ * output buffers; std_errors may be NULL. */
+typedef struct ltg_report {
+    double G;
+    double* means;               /* m */
+    double* lambda;              /* m */
+    double* grad;                /* M */
+    double* std_errors;          /* m, optional */
+    uint64_t paths;
+    uint64_t seed;
+    int32_t mode;
+} ltg_report;
+
+/* Device timings of the last compute call on a context (CUDA events on the
+ * context stream). */
+typedef struct ltg_timing {
+    double pass1_ms;             /* forward kernel(s) */
+    double pass2_ms;             /* adjoint kernel(s) */
+    double reduce_ms;            /* chunk reductions + finalisation + collectives */
+    double total_ms;
+    uint64_t paths_pass1;
+    uint64_t paths_pass2;
+    uint32_t launches;           /* kernels this library launched in the call */
+} ltg_timing;
+
+/* Path sharding plan: the path set is cut into fixed chunks whose size
+ * depends only on the total path count, so chunk partial sums and their
+ * ascending-order reduction are bitwise independent of the rank count. */
+typedef struct ltg_shard {
+    uint64_t chunk_paths;
+    uint64_t n_chunks;
+    uint64_t chunk_begin;        /* this rank's [chunk_begin, chunk_end) */
+    uint64_t chunk_end;
+    uint64_t path_begin;         /* [path_begin, path_end) of the global path index space */
+    uint64_t path_end;
+} ltg_shard;
+
+int ltg_abi_version(void);
+
+int ltg_create_heston(const ltg_heston_model* model, int device, ltg_ctx** out);
+int ltg_create_basket(const ltg_basket_model* model, int device, ltg_ctx** out);
+void ltg_destroy(ltg_ctx* ctx);
+const char* ltg_last_error(const ltg_ctx* ctx);
+
+size_t ltg_num_params(const ltg_ctx* ctx);   /* M */
+size_t ltg_num_outputs(const ltg_ctx* ctx);  /* m */
+size_t ltg_num_randoms(const ltg_ctx* ctx);  /* N per path */
+int ltg_pack_params(const ltg_ctx* ctx, double* x, size_t M);
+
+int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets, size_t m,
+                      const ltg_mc_config* cfg, ltg_report* report);
+int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg,
+                       double* means, double* std_errors);
+int ltg_finite_diff_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
+                                  size_t m, const ltg_mc_config* cfg, double h, double* grad);
+
+/* PhiloxNormalSource(seed, dim, antithetic).fill(path) for paths
+ * [path0, path0+npaths), generated on the GPU; out is npaths*dim, path-major. */
+int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, uint64_t path0,
+                     uint64_t npaths, double* out);
+
+int ltg_last_timing(const ltg_ctx* ctx, ltg_timing* out);
+
+/* 1 when the GPU inverse-normal uses a log() validated bit-for-bit against
+ * this host's libm (the reference's random stream is reproduced exactly);
+ * 0 when that check failed and the GPU fell back to CUDA's log(). */
+int ltg_rng_exact(const ltg_ctx* ctx);
+
+/* Multi-GPU (one process per GPU). Pure host arithmetic, no device use. */
+int ltg_shard_plan(uint64_t paths, int rank, int world, ltg_shard* out);
+/* NCCL is loaded at run time (the libnccl.so.2 already in the process, e.g.
+ * torch's, else the system one). Rank 0 creates the id, the caller
+ * broadcasts it, every rank attaches. After attach, compute calls shard the
+ * path set by ltg_shard_plan and all-gather chunk partials over NCCL; every
+ * rank returns the identical report. */
+int ltg_nccl_unique_id(unsigned char id[128]);
+int ltg_attach_nccl(ltg_ctx* ctx, const unsigned char id[128], int rank, int world);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LANETAPE_B200_H */

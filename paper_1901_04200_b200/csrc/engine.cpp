@@ -1,0 +1,762 @@
+// engine.cpp — host side of the C ABI (include/lanetape_b200.h).
+//
+// Orchestrates gradient_of_G (expectation.hpp:300-344) on one GPU or on one
+// rank of a multi-GPU job:
+//   pass 1  forward kernel over this rank's chunks      -> chunk partials, HBM checkpoints
+//   [NCCL all-gather of chunk partial rows]
+//   fixed-order chunk reduction -> means, std errors, lambda, G   (all on device)
+//   pass 2  adjoint kernel over the same chunks          -> chunk partials
+//   [NCCL all-gather]  fixed-order reduction -> grad = total / P
+//   one device->host copy of {G, means, se, lambda, grad}
+// Validation mirrors the reference's std::invalid_argument sites; a non-finite
+// result maps to LTG_ENUMERIC like EvalError.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lanetape_b200.h"
+#include "kernels.h"
+
+namespace ltg {
+bool discover_glibc_log(RngTables& t, std::string& why);
+void fill_as241(RngTables& t);
+}  // namespace ltg
+
+using namespace ltg;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Failure : std::runtime_error {
+    int code;
+    Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Failure(LTG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cuda_check(cudaMalloc(&p, b), "cudaMalloc");
+        bytes = b;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// ---- NCCL, resolved at run time ----
+struct Nccl {
+    void* lib = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+    bool load(std::string& why) {
+        if (lib) return true;
+        lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) {
+            why = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return false;
+        }
+        GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
+        CommInitRank = reinterpret_cast<decltype(CommInitRank)>(dlsym(lib, "ncclCommInitRank"));
+        AllGather = reinterpret_cast<decltype(AllGather)>(dlsym(lib, "ncclAllGather"));
+        CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(lib, "ncclCommDestroy"));
+        GetErrorString =
+            reinterpret_cast<decltype(GetErrorString)>(dlsym(lib, "ncclGetErrorString"));
+        if (!GetUniqueId || !CommInitRank || !AllGather || !CommDestroy || !GetErrorString) {
+            why = "libnccl.so.2 lacks required symbols";
+            return false;
+        }
+        return true;
+    }
+};
+Nccl& nccl() {
+    static Nccl n;
+    return n;
+}
+
+ltg_shard make_plan(uint64_t paths, int rank, int world) {
+    ltg_shard s{};
+    // chunk size depends on the total path count only
+    uint64_t r = paths / (uint64_t(8192) * kBlock);
+    uint64_t R = 1;
+    while (R * 2 <= r && R < 8) R *= 2;
+    s.chunk_paths = uint64_t(kBlock) * R;
+    s.n_chunks = (paths + s.chunk_paths - 1) / s.chunk_paths;
+    const uint64_t per = (s.n_chunks + world - 1) / world;  // padded equal split for all-gather
+    s.chunk_begin = std::min<uint64_t>(per * rank, s.n_chunks);
+    s.chunk_end = std::min<uint64_t>(per * (rank + 1), s.n_chunks);
+    s.path_begin = std::min<uint64_t>(s.chunk_begin * s.chunk_paths, paths);
+    s.path_end = std::min<uint64_t>(s.chunk_end * s.chunk_paths, paths);
+    return s;
+}
+
+uint64_t chunks_per_rank(const ltg_shard& s, int world) {
+    return (s.n_chunks + world - 1) / world;
+}
+
+}  // namespace
+
+struct ltg_ctx {
+    int kind = 0;  // 0 Heston SLV, 1 basket
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[8] = {};
+    std::string err;
+    std::string rng_note;
+
+    // model (host)
+    uint32_t steps = 0, cols = 1, rows = 1, nlev = 1, m = 0, M = 0, N = 0;
+    double s0 = 0, mu = 0, dt = 0;
+    std::vector<double> x0;
+    std::vector<MaturityEvent> events;
+    std::vector<uint32_t> inst_order;
+
+    // model (device)
+    DevBuf d_snodes, d_rowoff, d_events, d_order, d_strike, d_kind, d_rng;
+    RngTables h_rng{};
+
+    // per-call buffers
+    DevBuf d_x, d_targets, d_part1, d_part2, d_groups, d_tot1, d_tot2, d_res, d_grad, d_counter,
+        d_ckpt, d_normals;
+    double* h_stage = nullptr;  // pinned
+    size_t h_stage_bytes = 0;
+
+    // multi-GPU
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+
+    ltg_timing timing{};
+
+    ~ltg_ctx() {
+        if (comm) nccl().CommDestroy(comm);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (stream) cudaStreamDestroy(stream);
+        if (h_stage) cudaFreeHost(h_stage);
+    }
+
+    double* stage(size_t doubles) {
+        if (doubles * 8 > h_stage_bytes) {
+            if (h_stage) cudaFreeHost(h_stage);
+            h_stage = nullptr;
+            cuda_check(cudaMallocHost(&h_stage, doubles * 8), "cudaMallocHost");
+            h_stage_bytes = doubles * 8;
+        }
+        return h_stage;
+    }
+};
+
+namespace {
+
+template <typename Fn>
+int guarded(ltg_ctx* ctx, Fn&& fn) {
+    try {
+        if (ctx) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        fn();
+        return LTG_OK;
+    } catch (const Failure& f) {
+        if (ctx) ctx->err = f.what();
+        return f.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return LTG_ECUDA;
+    }
+}
+
+void require(bool ok, const std::string& msg) {
+    if (!ok) throw Failure(LTG_EINVAL, msg);
+}
+
+template <typename T>
+void upload(DevBuf& b, const std::vector<T>& v) {
+    b.ensure(std::max<size_t>(1, v.size()) * sizeof(T));
+    if (!v.empty())
+        cuda_check(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice),
+                   "upload");
+}
+
+void init_common(ltg_ctx* c, int device) {
+    int n = 0;
+    cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    require(device >= 0 && device < n, "device index out of range");
+    c->device = device;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+        throw Failure(LTG_ECUDA, std::string("device ") + prop.name +
+                                     " is not sm_100 (this library is built for sm_100a only)");
+    cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    for (auto& e : c->ev) cuda_check(cudaEventCreate(&e), "event");
+    fill_as241(c->h_rng);
+    std::string why;
+    if (!discover_glibc_log(c->h_rng, why)) c->rng_note = why;
+    c->d_rng.ensure(sizeof(RngTables));
+    cuda_check(cudaMemcpy(c->d_rng.p, &c->h_rng, sizeof(RngTables), cudaMemcpyHostToDevice),
+               "rng upload");
+    c->d_counter.ensure(64 * sizeof(uint32_t));
+}
+
+// maturity events from instrument maturity steps (stable order, like the
+// HestonSimulator bucketing, heston.hpp:524-539)
+void build_events(ltg_ctx* c, const std::vector<uint32_t>& mats) {
+    std::vector<uint32_t> order(mats.size());
+    std::iota(order.begin(), order.end(), 0u);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](uint32_t a, uint32_t b) { return mats[a] < mats[b]; });
+    c->events.clear();
+    for (uint32_t i = 0; i < order.size(); ++i) {
+        const uint32_t st = mats[order[i]];
+        if (c->events.empty() || c->events.back().step != st)
+            c->events.push_back(MaturityEvent{st, i, i + 1});
+        else
+            c->events.back().end = i + 1;
+    }
+    c->inst_order = order;
+    upload(c->d_events, c->events);
+    upload(c->d_order, c->inst_order);
+}
+
+size_t floor_index(const std::vector<double>& nodes, double x) {
+    auto it = std::upper_bound(nodes.begin(), nodes.end(), x);
+    return it == nodes.begin() ? 0 : size_t(it - nodes.begin() - 1);
+}
+
+void all_gather_rows(ltg_ctx* c, double* table, uint64_t per_rank, uint32_t width) {
+    if (c->world <= 1) return;
+    const size_t count = size_t(per_rank) * width;
+    const ncclResult_t r = nccl().AllGather(table + size_t(c->rank) * count, table, count,
+                                            ncclFloat64, c->comm, c->stream);
+    if (r != ncclSuccess)
+        throw Failure(LTG_ECUDA, std::string("ncclAllGather: ") + nccl().GetErrorString(r));
+}
+
+struct Pass1Out {
+    bool have_ckpt = false;
+};
+
+HestonArgs heston_args(ltg_ctx* c) {
+    HestonArgs a{};
+    a.steps = c->steps;
+    a.cols = c->cols;
+    a.rows = c->rows;
+    a.nlev = c->nlev;
+    a.m = c->m;
+    a.n_events = (uint32_t)c->events.size();
+    a.s0 = c->s0;
+    a.dt = c->dt;
+    a.sqdt = std::sqrt(c->dt);
+    a.mu_dt = c->mu * c->dt;
+    a.half_dt = 0.5 * c->dt;
+    a.x = c->d_x.as<double>();
+    a.s_nodes = c->d_snodes.as<double>();
+    a.row_off = c->d_rowoff.as<uint16_t>();
+    a.events = c->d_events.as<MaturityEvent>();
+    a.inst_order = c->d_order.as<uint32_t>();
+    a.strike = c->d_strike.as<double>();
+    a.kind = c->d_kind.as<int32_t>();
+    a.rng = c->d_rng.as<RngTables>();
+    return a;
+}
+
+Work base_work(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan) {
+    Work w{};
+    w.paths = cfg.paths;
+    w.path_offset = 0;
+    w.chunk_paths = plan.chunk_paths;
+    w.chunk_begin = plan.chunk_begin;
+    w.n_chunks = plan.chunk_end - plan.chunk_begin;
+    w.ckpt_path0 = plan.path_begin;
+    w.ckpt_stride = std::max<uint64_t>(1, plan.path_end - plan.path_begin);
+    w.counter = c->d_counter.as<uint32_t>();
+    w.seed_lo = (uint32_t)cfg.seed;
+    w.seed_hi = (uint32_t)(cfg.seed >> 32);
+    w.antithetic = cfg.antithetic ? 1 : 0;
+    return w;
+}
+
+void zero_counter(ltg_ctx* c, int slot) {
+    cuda_check(cudaMemsetAsync(c->d_counter.as<uint32_t>() + slot, 0, sizeof(uint32_t), c->stream),
+               "memset");
+}
+
+void validate_cfg(ltg_ctx* c, const ltg_mc_config* cfg, size_t M) {
+    require(cfg != nullptr, "null MCConfig");
+    require(M == c->M, "parameter vector has " + std::to_string(M) + " entries, program has " +
+                           std::to_string(c->M));
+    require(cfg->paths > 0, "forward_pass: paths must be > 0");
+    require(cfg->precision == LTG_FP64 || cfg->precision == LTG_FP32, "unknown precision");
+    require(cfg->precision == LTG_FP64, "fp32 precision is not available for this model yet");
+}
+
+void check_params(ltg_ctx* c, const double* x) {
+    for (size_t j = 0; j < c->M; ++j)
+        if (!std::isfinite(x[j])) throw Failure(LTG_ENUMERIC, "non-finite parameter");
+    if (c->kind == 0 && !(1.0 - x[3] * x[3] >= 0.0))
+        throw Failure(LTG_ENUMERIC, "sqrt of negative value (1 - rho^2)");
+}
+
+// Pass 1 over this rank's chunks (+ all-gather) and the fixed-order reduction
+// into d_res = [G, means, se, lambda]. Returns whether pass-2 checkpoints of the
+// step-1 path set were written.
+bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool targets,
+               bool want_ckpt) {
+    const uint64_t per = chunks_per_rank(plan, c->world);
+    const uint64_t table_rows = per * c->world;
+    const uint32_t width = 2 * c->m;
+    c->d_part1.ensure(table_rows * width * 8);
+    c->d_groups.ensure(((plan.n_chunks + kGroup - 1) / kGroup) * std::max(width, c->M) * 8 + 8);
+    c->d_tot1.ensure(width * 8);
+    c->d_res.ensure((1 + 3 * c->m) * 8);
+
+    HestonArgs a = heston_args(c);
+    Work w = base_work(c, cfg, plan);
+    const uint32_t nseg = (c->steps + kSegSteps - 1) / kSegSteps;
+    bool ckpt = false;
+    if (want_ckpt && nseg > 1) {
+        const size_t need = size_t(nseg - 1) * w.ckpt_stride * 16;
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        if (need <= c->d_ckpt.bytes || need + (size_t(2) << 30) < free_b) {
+            c->d_ckpt.ensure(need);
+            ckpt = true;
+        }
+    }
+    a.partials = c->d_part1.as<double>() + plan.chunk_begin * width;
+    a.ckpt = ckpt ? c->d_ckpt.as<double2>() : nullptr;
+    a.write_sums = 1;
+    a.write_ckpt = ckpt ? 1 : 0;
+    // partial rows are indexed from the launch's first chunk
+    zero_counter(c, 0);
+    cuda_check(cudaEventRecord(c->ev[0], c->stream), "event");
+    if (w.n_chunks) cuda_check(launch_heston_pass1(a, w, 0, c->stream), "heston pass 1");
+    cuda_check(cudaEventRecord(c->ev[1], c->stream), "event");
+    c->timing.launches += w.n_chunks ? 1 : 0;
+    all_gather_rows(c, c->d_part1.as<double>(), per, width);
+    cuda_check(launch_reduce_chunks(c->d_part1.as<double>(), plan.n_chunks, width,
+                                    c->d_groups.as<double>(), c->d_tot1.as<double>(), c->stream),
+               "reduce");
+    cuda_check(launch_finalize_means(c->d_tot1.as<double>(), c->m, cfg.paths,
+                                     targets ? c->d_targets.as<double>() : nullptr,
+                                     c->d_res.as<double>(), c->stream),
+               "finalize");
+    cuda_check(cudaEventRecord(c->ev[2], c->stream), "event");
+    c->timing.launches += 3;
+    c->timing.paths_pass1 = plan.path_end - plan.path_begin;
+    return ckpt;
+}
+
+void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool have_ckpt) {
+    const uint64_t per = chunks_per_rank(plan, c->world);
+    const uint64_t table_rows = per * c->world;
+    c->d_part2.ensure(table_rows * c->M * 8);
+    c->d_tot2.ensure(c->M * 8);
+    c->d_grad.ensure(c->M * 8);
+    HestonArgs a = heston_args(c);
+    a.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
+    Work w = base_work(c, cfg, plan);
+    const uint32_t nseg = (c->steps + kSegSteps - 1) / kSegSteps;
+    cuda_check(cudaEventRecord(c->ev[3], c->stream), "event");
+    if (w.n_chunks) {
+        if (!have_ckpt && nseg > 1) {
+            // fresh_step2_paths or no room for a full checkpoint table: replay
+            // the pass-2 path set in waves (checkpoint-only forward, then adjoint)
+            if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            const size_t per_chunk = size_t(nseg - 1) * plan.chunk_paths * 16;
+            size_t budget = c->d_ckpt.bytes;
+            if (budget < per_chunk * 64 && free_b > (size_t(2) << 30))
+                budget = std::max(budget, std::min(free_b - (size_t(2) << 30),
+                                                   per_chunk * w.n_chunks));
+            uint64_t wave = std::max<uint64_t>(1, budget / per_chunk);
+            wave = std::min<uint64_t>(wave, w.n_chunks);
+            c->d_ckpt.ensure(wave * per_chunk);
+            for (uint64_t c0 = 0; c0 < w.n_chunks; c0 += wave) {
+                Work ww = w;
+                ww.chunk_begin = w.chunk_begin + c0;
+                ww.n_chunks = std::min<uint64_t>(wave, w.n_chunks - c0);
+                ww.ckpt_path0 = ww.chunk_begin * plan.chunk_paths;
+                ww.ckpt_stride = ww.n_chunks * plan.chunk_paths;
+                HestonArgs r = a;
+                r.ckpt = c->d_ckpt.as<double2>();
+                r.write_sums = 0;
+                r.write_ckpt = 1;
+                r.partials = nullptr;
+                zero_counter(c, 1);
+                ww.counter = c->d_counter.as<uint32_t>() + 1;
+                cuda_check(launch_heston_pass1(r, ww, 0, c->stream), "heston replay");
+                HestonArgs b = a;
+                b.ckpt = c->d_ckpt.as<double2>();
+                b.partials = c->d_part2.as<double>() + ww.chunk_begin * c->M;
+                zero_counter(c, 2);
+                ww.counter = c->d_counter.as<uint32_t>() + 2;
+                cuda_check(launch_heston_pass2(b, ww, 0, c->stream), "heston pass 2");
+                c->timing.launches += 2;
+            }
+        } else {
+            if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
+            a.ckpt = c->d_ckpt.as<double2>();
+            a.partials = c->d_part2.as<double>() + plan.chunk_begin * c->M;
+            zero_counter(c, 2);
+            w.counter = c->d_counter.as<uint32_t>() + 2;
+            cuda_check(launch_heston_pass2(a, w, 0, c->stream), "heston pass 2");
+            c->timing.launches += 1;
+        }
+    }
+    cuda_check(cudaEventRecord(c->ev[4], c->stream), "event");
+    all_gather_rows(c, c->d_part2.as<double>(), per, c->M);
+    cuda_check(launch_reduce_chunks(c->d_part2.as<double>(), plan.n_chunks, c->M,
+                                    c->d_groups.as<double>(), c->d_tot2.as<double>(), c->stream),
+               "reduce");
+    cuda_check(launch_finalize_grad(c->d_tot2.as<double>(), c->M, cfg.paths,
+                                    c->d_grad.as<double>(), c->stream),
+               "finalize grad");
+    cuda_check(cudaEventRecord(c->ev[5], c->stream), "event");
+    c->timing.launches += 3;
+    c->timing.paths_pass2 = plan.path_end - plan.path_begin;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+void upload_x(ltg_ctx* c, const double* x, const double* targets) {
+    const size_t n = c->M + (targets ? c->m : 0);
+    double* st = c->stage(n);
+    std::memcpy(st, x, c->M * 8);
+    if (targets) std::memcpy(st + c->M, targets, c->m * 8);
+    c->d_x.ensure(c->M * 8);
+    cuda_check(cudaMemcpyAsync(c->d_x.p, st, c->M * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    if (targets) {
+        c->d_targets.ensure(c->m * 8);
+        cuda_check(cudaMemcpyAsync(c->d_targets.p, st + c->M, c->m * 8, cudaMemcpyHostToDevice,
+                                   c->stream),
+                   "H2D");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ltg_abi_version(void) { return LTG_ABI_VERSION; }
+
+int ltg_create_heston(const ltg_heston_model* mdl, int device, ltg_ctx** out) {
+    if (!out || !mdl) {
+        g_create_error = "null argument";
+        return LTG_EINVAL;
+    }
+    *out = nullptr;
+    auto c = std::make_unique<ltg_ctx>();
+    const int rc = guarded(c.get(), [&] {
+        const ltg_heston_model& m = *mdl;
+        // validate(ModelSpec) minus McSettings.paths (heston.hpp:199-299)
+        require(m.s0 > 0.0, "HestonParams: s0 must be > 0");
+        require(m.v0 >= 0.0, "HestonParams: v0 must be >= 0");
+        require(m.theta >= 0.0, "HestonParams: theta must be >= 0");
+        require(m.kappa >= 0.0, "HestonParams: kappa must be >= 0");
+        require(m.xi >= 0.0, "HestonParams: xi must be >= 0");
+        require(std::fabs(m.rho) < 1.0, "HestonParams: rho must satisfy |rho| < 1");
+        require(std::isfinite(m.mu), "HestonParams: mu must be finite");
+        require(m.n_t_nodes > 0 && m.n_s_nodes > 0 && m.t_nodes && m.s_nodes,
+                "LeverageGrid: node lists must be non-empty");
+        for (uint32_t i = 1; i < m.n_t_nodes; ++i)
+            require(m.t_nodes[i] > m.t_nodes[i - 1], "LeverageGrid: t_nodes must be strictly ascending");
+        for (uint32_t i = 1; i < m.n_s_nodes; ++i)
+            require(m.s_nodes[i] > m.s_nodes[i - 1], "LeverageGrid: s_nodes must be strictly ascending");
+        const uint32_t nlev = m.n_t_nodes * m.n_s_nodes;
+        require(m.leverage != nullptr, "LeverageGrid: values must hold t_nodes x s_nodes entries");
+        for (uint32_t i = 0; i < nlev; ++i)
+            require(std::isfinite(m.leverage[i]) && m.leverage[i] >= 0.0,
+                    "LeverageGrid: values must be finite and >= 0");
+        require(m.steps > 0, "mc: steps must be > 0");
+        require(m.dt > 0.0, "mc: dt must be > 0");
+        require(m.n_instruments > 0, "instruments: list must be non-empty");
+        for (uint32_t i = 0; i < m.n_instruments; ++i) {
+            require(m.inst_strike[i] > 0.0,
+                    "instruments[" + std::to_string(i) + "]: strike must be > 0");
+            require(m.inst_maturity_step[i] >= 1 && m.inst_maturity_step[i] <= m.steps,
+                    "instruments[" + std::to_string(i) + "]: maturity_step must be in [1, steps]");
+            require(m.inst_kind[i] == LTG_CALL || m.inst_kind[i] == LTG_PUT,
+                    "instruments: kind must be call or put");
+        }
+        // device limits of this build
+        require(m.n_s_nodes <= kMaxCols, "GPU build supports at most 8 s-nodes");
+        require(nlev <= kMaxLev, "GPU build supports at most 1024 leverage cells");
+        require(m.n_instruments <= kMaxInstruments, "GPU build supports at most 256 instruments");
+        require(m.steps <= 65535 && (uint64_t)(m.n_t_nodes - 1) * m.n_s_nodes < 65536,
+                "GPU build supports at most 65535 steps");
+
+        init_common(c.get(), device);
+        c->kind = 0;
+        c->steps = m.steps;
+        c->cols = m.n_s_nodes;
+        c->rows = m.n_t_nodes;
+        c->nlev = nlev;
+        c->m = m.n_instruments;
+        c->M = 5 + nlev;
+        c->N = 2 * m.steps;
+        c->s0 = m.s0;
+        c->mu = m.mu;
+        c->dt = m.dt;
+        c->x0 = {m.kappa, m.theta, m.xi, m.rho, m.v0};
+        c->x0.insert(c->x0.end(), m.leverage, m.leverage + nlev);
+        std::vector<double> tn(m.t_nodes, m.t_nodes + m.n_t_nodes);
+        std::vector<uint16_t> rowoff(m.steps);
+        for (uint32_t k = 0; k < m.steps; ++k)
+            rowoff[k] = (uint16_t)(floor_index(tn, (double)k * m.dt) * m.n_s_nodes);
+        upload(c->d_rowoff, rowoff);
+        upload(c->d_snodes, std::vector<double>(m.s_nodes, m.s_nodes + m.n_s_nodes));
+        upload(c->d_strike, std::vector<double>(m.inst_strike, m.inst_strike + m.n_instruments));
+        upload(c->d_kind, std::vector<int32_t>(m.inst_kind, m.inst_kind + m.n_instruments));
+        build_events(c.get(), std::vector<uint32_t>(m.inst_maturity_step,
+                                                     m.inst_maturity_step + m.n_instruments));
+        cuda_check(cudaDeviceSynchronize(), "init");
+    });
+    if (rc != LTG_OK) {
+        g_create_error = c->err;
+        return rc;
+    }
+    *out = c.release();
+    return LTG_OK;
+}
+
+int ltg_create_basket(const ltg_basket_model* mdl, int device, ltg_ctx** out) {
+    (void)mdl;
+    (void)device;
+    if (out) *out = nullptr;
+    g_create_error = "basket model not available in this build";
+    return LTG_EINVAL;
+}
+
+void ltg_destroy(ltg_ctx* ctx) { delete ctx; }
+
+const char* ltg_last_error(const ltg_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+size_t ltg_num_params(const ltg_ctx* ctx) { return ctx ? ctx->M : 0; }
+size_t ltg_num_outputs(const ltg_ctx* ctx) { return ctx ? ctx->m : 0; }
+size_t ltg_num_randoms(const ltg_ctx* ctx) { return ctx ? ctx->N : 0; }
+
+int ltg_pack_params(const ltg_ctx* ctx, double* x, size_t M) {
+    if (!ctx || !x || M != ctx->M) return LTG_EINVAL;
+    std::copy(ctx->x0.begin(), ctx->x0.end(), x);
+    return LTG_OK;
+}
+
+int ltg_rng_exact(const ltg_ctx* ctx) { return ctx ? ctx->h_rng.exact : 0; }
+
+int ltg_shard_plan(uint64_t paths, int rank, int world, ltg_shard* out) {
+    if (!out || world < 1 || rank < 0 || rank >= world || paths == 0) return LTG_EINVAL;
+    *out = make_plan(paths, rank, world);
+    return LTG_OK;
+}
+
+int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets, size_t m,
+                      const ltg_mc_config* cfg, ltg_report* report) {
+    if (!ctx) return LTG_EINVAL;
+    return guarded(ctx, [&] {
+        validate_cfg(ctx, cfg, M);
+        require(x && targets && report && report->means && report->lambda && report->grad,
+                "null buffer");
+        require(m == ctx->m, "gradient_of_G: " + std::to_string(m) + " targets for " +
+                                 std::to_string(ctx->m) + " outputs");
+        require(!(cfg->memory_mode == LTG_MODE_STORE && cfg->fresh_step2_paths),
+                "gradient_of_G: fresh_step2_paths replays nothing, so stored forward state "
+                "cannot be used; switch to recompute mode");
+        check_params(ctx, x);
+        ctx->timing = ltg_timing{};
+        const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
+        upload_x(ctx, x, targets);
+        const bool ckpt = run_pass1(ctx, *cfg, plan, true, !cfg->fresh_step2_paths);
+        run_pass2(ctx, *cfg, plan, ckpt);
+        const uint32_t nm = ctx->m;
+        double* st = ctx->stage(1 + 3 * nm + ctx->M);
+        cuda_check(cudaMemcpyAsync(st, ctx->d_res.p, (1 + 3 * nm) * 8, cudaMemcpyDeviceToHost,
+                                   ctx->stream),
+                   "D2H");
+        cuda_check(cudaMemcpyAsync(st + 1 + 3 * nm, ctx->d_grad.p, ctx->M * 8,
+                                   cudaMemcpyDeviceToHost, ctx->stream),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "gradient_of_G");
+        ctx->timing.pass1_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+        ctx->timing.pass2_ms = elapsed(ctx->ev[3], ctx->ev[4]);
+        ctx->timing.reduce_ms = elapsed(ctx->ev[1], ctx->ev[2]) + elapsed(ctx->ev[4], ctx->ev[5]);
+        ctx->timing.total_ms = elapsed(ctx->ev[0], ctx->ev[5]);
+        report->G = st[0];
+        std::memcpy(report->means, st + 1, nm * 8);
+        if (report->std_errors) std::memcpy(report->std_errors, st + 1 + nm, nm * 8);
+        std::memcpy(report->lambda, st + 1 + 2 * nm, nm * 8);
+        std::memcpy(report->grad, st + 1 + 3 * nm, ctx->M * 8);
+        report->paths = cfg->paths;
+        report->seed = cfg->seed;
+        report->mode = cfg->memory_mode;
+        bool finite = std::isfinite(report->G);
+        for (size_t j = 0; j < ctx->M; ++j) finite = finite && std::isfinite(report->grad[j]);
+        if (!finite) throw Failure(LTG_ENUMERIC, "gradient_of_G: non-finite result");
+    });
+}
+
+int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg,
+                       double* means, double* std_errors) {
+    if (!ctx) return LTG_EINVAL;
+    return guarded(ctx, [&] {
+        validate_cfg(ctx, cfg, M);
+        require(x && means, "null buffer");
+        check_params(ctx, x);
+        ctx->timing = ltg_timing{};
+        const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
+        upload_x(ctx, x, nullptr);
+        run_pass1(ctx, *cfg, plan, false, false);
+        const uint32_t nm = ctx->m;
+        double* st = ctx->stage(1 + 3 * nm);
+        cuda_check(cudaMemcpyAsync(st, ctx->d_res.p, (1 + 3 * nm) * 8, cudaMemcpyDeviceToHost,
+                                   ctx->stream),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "estimate_means");
+        ctx->timing.pass1_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+        ctx->timing.reduce_ms = elapsed(ctx->ev[1], ctx->ev[2]);
+        ctx->timing.total_ms = elapsed(ctx->ev[0], ctx->ev[2]);
+        std::memcpy(means, st + 1, nm * 8);
+        if (std_errors) std::memcpy(std_errors, st + 1 + nm, nm * 8);
+        for (uint32_t o = 0; o < nm; ++o)
+            if (!std::isfinite(means[o]))
+                throw Failure(LTG_ENUMERIC, "estimate_means: non-finite result");
+    });
+}
+
+int ltg_finite_diff_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
+                                  size_t m, const ltg_mc_config* cfg, double h, double* grad) {
+    if (!ctx) return LTG_EINVAL;
+    if (!(h > 0.0)) {
+        ctx->err = "finite_diff_gradient_of_G: h must be > 0";
+        return LTG_EINVAL;
+    }
+    if (!x || !targets || !grad || M != ctx->M || m != ctx->m) {
+        ctx->err = "finite_diff_gradient_of_G: size mismatch";
+        return LTG_EINVAL;
+    }
+    // expectation.hpp:372-400: central differences of G under common random numbers
+    std::vector<double> xv(x, x + M), means(m);
+    auto G_at = [&](double& out) {
+        const int rc = ltg_estimate_means(ctx, xv.data(), M, cfg, means.data(), nullptr);
+        if (rc) return rc;
+        double g = 0.0;
+        for (size_t o = 0; o < m; ++o) {
+            const double l = means[o] - targets[o];
+            g += 0.5 * l * l;
+        }
+        out = g;
+        return 0;
+    };
+    for (size_t j = 0; j < M; ++j) {
+        const double saved = xv[j];
+        double up = 0, down = 0;
+        xv[j] = saved + h;
+        int rc = G_at(up);
+        if (rc) return rc;
+        xv[j] = saved - h;
+        rc = G_at(down);
+        if (rc) return rc;
+        xv[j] = saved;
+        grad[j] = (up - down) / (2.0 * h);
+    }
+    return LTG_OK;
+}
+
+int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, uint64_t path0,
+                     uint64_t npaths, double* out) {
+    if (!ctx) return LTG_EINVAL;
+    return guarded(ctx, [&] {
+        require(out != nullptr, "null buffer");
+        require(dim > 0 && dim < (size_t(1) << 30), "dimension out of range");
+        const size_t n = size_t(npaths) * dim;
+        if (n == 0) return;
+        ctx->d_normals.ensure(n * 8);
+        cuda_check(launch_fill_normals(ctx->d_rng.as<RngTables>(), (uint32_t)seed,
+                                       (uint32_t)(seed >> 32), antithetic, path0, npaths,
+                                       (uint32_t)dim, ctx->d_normals.as<double>(), ctx->stream),
+                   "fill_normals");
+        cuda_check(cudaMemcpyAsync(out, ctx->d_normals.p, n * 8, cudaMemcpyDeviceToHost,
+                                   ctx->stream),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "fill_normals");
+    });
+}
+
+int ltg_last_timing(const ltg_ctx* ctx, ltg_timing* out) {
+    if (!ctx || !out) return LTG_EINVAL;
+    *out = ctx->timing;
+    return LTG_OK;
+}
+
+int ltg_nccl_unique_id(unsigned char id[128]) {
+    std::string why;
+    if (!nccl().load(why)) {
+        g_create_error = why;
+        return LTG_ECUDA;
+    }
+    ncclUniqueId u;
+    const ncclResult_t r = nccl().GetUniqueId(&u);
+    if (r != ncclSuccess) {
+        g_create_error = nccl().GetErrorString(r);
+        return LTG_ECUDA;
+    }
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, 128);
+    return LTG_OK;
+}
+
+int ltg_attach_nccl(ltg_ctx* ctx, const unsigned char id[128], int rank, int world) {
+    if (!ctx) return LTG_EINVAL;
+    return guarded(ctx, [&] {
+        require(id != nullptr && world >= 1 && rank >= 0 && rank < world, "bad rank/world");
+        std::string why;
+        if (!nccl().load(why)) throw Failure(LTG_ECUDA, why);
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        if (ctx->comm) nccl().CommDestroy(ctx->comm);
+        ctx->comm = nullptr;
+        const ncclResult_t r = nccl().CommInitRank(&ctx->comm, world, u, rank);
+        if (r != ncclSuccess)
+            throw Failure(LTG_ECUDA, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+        ctx->rank = rank;
+        ctx->world = world;
+    });
+}
+
+}  // extern "C"

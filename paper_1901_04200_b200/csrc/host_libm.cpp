@@ -1,0 +1,177 @@
+// host_libm.cpp — makes the GPU's log() reproduce the host libm bit for bit.
+//
+// The reference draws its normals with glibc's log() (rng.hpp:61) on the host
+// that runs it. glibc >= 2.28 implements log() with the ARM optimized-routines
+// algorithm (x = 2^k z, 128-entry (1/c, log c) table, degree-5 polynomial in
+// r = z/c - 1); on x86-64 CPUs with FMA the ifunc selects the FMA build,
+// whose operation sequence rng.cuh:glibc_log restates. Glibc rounds the
+// wrong way for about 1 in 10^4 tail arguments, so a correctly rounded (or
+// CUDA) log would change some reference draws in the last bit.
+//
+// The table is not shipped with this library: at context creation we locate
+// the `__log_data` block inside the libm this process already loaded (by its
+// ln2hi/ln2lo header), then VALIDATE it by evaluating the restated sequence
+// on the host against the real log() over 65,536 arguments spanning every
+// table interval of the tail domain. Only a table that reproduces log()
+// bit-for-bit on all of them is used (RngTables::exact = 1); otherwise the GPU
+// falls back to CUDA's log() and ltg_rng_exact() reports 0.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace ltg {
+
+namespace {
+
+double bits2d(uint64_t u) {
+    double d;
+    std::memcpy(&d, &u, 8);
+    return d;
+}
+uint64_t d2bits(double d) {
+    uint64_t u;
+    std::memcpy(&u, &d, 8);
+    return u;
+}
+
+// host restatement of rng.cuh:glibc_log (std::fma == __fma_rn bit for bit)
+double emulate_log(const RngTables& t, double x) {
+    const uint64_t ix = d2bits(x);
+    const uint64_t tmp = ix - 0x3fe6000000000000ULL;
+    const int i = (int)((tmp >> 45) & 127);
+    const int k = (int)((int64_t)tmp >> 52);
+    const double z = bits2d(ix - (tmp & 0xfff0000000000000ULL));
+    const double invc = t.log_tab[i].x, logc = t.log_tab[i].y;
+    const double kd = (double)k;
+    const double w = std::fma(kd, t.log_ln2hi, logc);
+    const double r = std::fma(z, invc, -1.0);
+    const double p12 = std::fma(r, t.log_poly[2], t.log_poly[1]);
+    volatile double hi = r + w;
+    volatile double r2 = r * r;
+    volatile double wh = w - hi;
+    volatile double whr = wh + r;
+    const double lo = std::fma(kd, t.log_ln2lo, whr);
+    volatile double r3 = r * r2;
+    const double p34 = std::fma(r, t.log_poly[4], t.log_poly[3]);
+    const double lo2 = std::fma(r2, t.log_poly[0], lo);
+    const double p = std::fma(p34, r2, p12);
+    const double y = std::fma(r3, p, lo2);
+    volatile double out = y + hi;
+    return out;
+}
+
+bool read_file(const char* path, std::vector<unsigned char>& buf) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return false;
+    buf.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+    return !buf.empty();
+}
+
+// arguments of log() on the reference's tail path: min(p, 1-p) with
+// p = (2n+1) 2^-53, i.e. x in [2^-53, 0.075]
+bool validate(const RngTables& t) {
+    uint64_t s = 0x9E3779B97F4A7C15ULL;
+    for (int i = 0; i < 65536; ++i) {
+        s ^= s << 13;
+        s ^= s >> 7;
+        s ^= s << 17;
+        double x;
+        if (i < 4096) {
+            // every table interval, both binade halves, at several exponents
+            const int e = -(int)(i % 54) - 1;
+            const uint64_t mant = ((uint64_t)(i / 54) << 45) ^ (s & ((1ULL << 45) - 1));
+            x = std::ldexp(bits2d(0x3ff0000000000000ULL | (mant & 0xfffffffffffffULL)), e);
+        } else {
+            const uint64_t n = s >> 12;  // 52-bit integer
+            x = ((double)(2 * n + 1)) * 0x1p-53;
+            if (x > 0.5) x = 1.0 - x;
+        }
+        if (!(x > 0.0) || x > 0.075) continue;
+        if (emulate_log(t, x) != std::log(x)) return false;
+    }
+    return true;
+}
+
+}  // namespace
+
+// Fills the log part of `t`. Returns true (t.exact = 1) when a validated
+// table was found; `why` explains a failure.
+bool discover_glibc_log(RngTables& t, std::string& why) {
+    t.exact = 0;
+    Dl_info info;
+    void* sym = dlsym(RTLD_DEFAULT, "log");
+    if (!sym || !dladdr(sym, &info) || !info.dli_fname) {
+        why = "cannot locate the libm that provides log()";
+        return false;
+    }
+    std::vector<unsigned char> buf;
+    if (!read_file(info.dli_fname, buf)) {
+        why = std::string("cannot read ") + info.dli_fname;
+        return false;
+    }
+    const uint64_t ln2hi = d2bits(0x1.62e42fefa3800p-1), ln2lo = d2bits(0x1.ef35793c76730p-45);
+    // struct log_data { ln2hi, ln2lo, poly[5], poly1[11], tab[128]{invc, logc}, tab2[128] }
+    const size_t need = (2 + 5 + 11 + 256) * 8;
+    for (size_t off = 0; off + need <= buf.size(); off += 8) {
+        uint64_t a, b;
+        std::memcpy(&a, &buf[off], 8);
+        if (a != ln2hi) continue;
+        std::memcpy(&b, &buf[off + 8], 8);
+        if (b != ln2lo) continue;
+        RngTables cand = t;
+        const double* d = reinterpret_cast<const double*>(&buf[off]);
+        double tmp[2 + 5 + 11 + 256];
+        std::memcpy(tmp, d, sizeof tmp);
+        cand.log_ln2hi = tmp[0];
+        cand.log_ln2lo = tmp[1];
+        for (int i = 0; i < 5; ++i) cand.log_poly[i] = tmp[2 + i];
+        for (int i = 0; i < 128; ++i) {
+            cand.log_tab[i].x = tmp[18 + 2 * i];
+            cand.log_tab[i].y = tmp[18 + 2 * i + 1];
+        }
+        if (validate(cand)) {
+            cand.exact = 1;
+            t = cand;
+            return true;
+        }
+    }
+    why = std::string("no log table in ") + info.dli_fname +
+          " reproduces log() bit for bit; using CUDA log()";
+    return false;
+}
+
+// AS241 coefficient rows (rng.hpp:49-58, 65-72, 75-82), highest degree first;
+// the denominators' constant terms are 1.0.
+void fill_as241(RngTables& t) {
+    static const double num[3][8] = {
+        {2.5090809287301226727e+3, 3.3430575583588128105e+4, 6.7265770927008700853e+4,
+         4.5921953931549871457e+4, 1.3731693765509461125e+4, 1.9715909503065514427e+3,
+         1.3314166789178437745e+2, 3.3871328727963666080e+0},
+        {7.74545014278341407640e-4, 2.27238449892691845833e-2, 2.41780725177450611770e-1,
+         1.27045825245236838258e+0, 3.64784832476320460504e+0, 5.76949722146069140550e+0,
+         4.63033784615654529590e+0, 1.42343711074968357734e+0},
+        {2.01033439929228813265e-7, 2.71155556874348757815e-5, 1.24266094738807843860e-3,
+         2.65321895265761230930e-2, 2.96560571828504891230e-1, 1.78482653991729133580e+0,
+         5.46378491116411436990e+0, 6.65790464350110377720e+0}};
+    static const double den[3][8] = {
+        {5.2264952788528545610e+3, 2.8729085735721942674e+4, 3.9307895800092710610e+4,
+         2.1213794301586595867e+4, 5.3941960214247511077e+3, 6.8718700749205790830e+2,
+         4.2313330701600911252e+1, 1.0},
+        {1.05075007164441684324e-9, 5.47593808499534494600e-4, 1.51986665636164571966e-2,
+         1.48103976427480074590e-1, 6.89767334985100004550e-1, 1.67638483018380384940e+0,
+         2.05319162663775882187e+0, 1.0},
+        {2.04426310338993978564e-15, 1.42151175831644588870e-7, 1.84631831751005468180e-5,
+         7.86869131145613259100e-4, 1.48753612908506148525e-2, 1.36929880922735805310e-1,
+         5.99832206555887937690e-1, 1.0}};
+    for (int s = 0; s < 3; ++s)
+        for (int k = 0; k < 8; ++k) t.coef[s][k] = make_double2(num[s][k], den[s][k]);
+}
+
+}  // namespace ltg

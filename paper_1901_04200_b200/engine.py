@@ -1,0 +1,224 @@
+"""Python binding of the CUDA engine's C ABI (include/lanetape_b200.h).
+
+Mirrors the reference's calling surface (expectation.hpp): ``gradient_of_G``,
+``estimate_means``, ``finite_diff_gradient_of_G`` returning ``GradientReport`` /
+``MeansResult``; ``Objective`` factories for the reference's calibrator
+(calibrate.hpp:117-120). There is no CPU fallback: if the built library
+(``_lib/liblanetape_b200.so``) is missing or no sm_100 GPU is usable, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import cabi
+from .cabi import (LTG_ECUDA, LTG_EINVAL, LTG_ENUMERIC, MarshalledModel, MCConfigC, ReportC,
+                   ShardC, TimingC)
+from .model import GradientReport, MCConfig, MeansResult, memory_mode_name
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                        "liblanetape_b200.so")
+
+_dp = C.POINTER(C.c_double)
+
+
+class EvalError(RuntimeError):
+    """Numerical failure (the reference's lanetape::EvalError)."""
+
+
+class EngineError(RuntimeError):
+    """CUDA / NCCL failure."""
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise EngineError(f"CUDA engine library not built: {path} (run __graft_entry__.build())")
+    L = C.CDLL(path)
+    L.ltg_abi_version.restype = C.c_int
+    L.ltg_create_heston.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+    L.ltg_create_basket.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+    L.ltg_destroy.argtypes = [C.c_void_p]
+    L.ltg_last_error.argtypes = [C.c_void_p]
+    L.ltg_last_error.restype = C.c_char_p
+    for f in ("ltg_num_params", "ltg_num_outputs", "ltg_num_randoms"):
+        getattr(L, f).argtypes = [C.c_void_p]
+        getattr(L, f).restype = C.c_size_t
+    L.ltg_pack_params.argtypes = [C.c_void_p, _dp, C.c_size_t]
+    L.ltg_gradient_of_G.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, C.c_size_t,
+                                    C.POINTER(MCConfigC), C.POINTER(ReportC)]
+    L.ltg_estimate_means.argtypes = [C.c_void_p, _dp, C.c_size_t, C.POINTER(MCConfigC), _dp, _dp]
+    L.ltg_finite_diff_gradient_of_G.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, C.c_size_t,
+                                                C.POINTER(MCConfigC), C.c_double, _dp]
+    L.ltg_fill_normals.argtypes = [C.c_void_p, C.c_uint64, C.c_size_t, C.c_int, C.c_uint64,
+                                   C.c_uint64, _dp]
+    L.ltg_last_timing.argtypes = [C.c_void_p, C.POINTER(TimingC)]
+    L.ltg_rng_exact.argtypes = [C.c_void_p]
+    L.ltg_shard_plan.argtypes = [C.c_uint64, C.c_int, C.c_int, C.POINTER(ShardC)]
+    L.ltg_nccl_unique_id.argtypes = [C.c_char_p]
+    L.ltg_attach_nccl.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int]
+    _lib = L
+    return L
+
+
+def _arr(x: Sequence[float]) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _cfg(cfg: MCConfig) -> MCConfigC:
+    return MCConfigC(int(cfg.paths), int(cfg.seed) & 0xFFFFFFFFFFFFFFFF, int(bool(cfg.antithetic)),
+                     int(bool(cfg.fresh_step2_paths)), int(cfg.memory_mode), int(cfg.precision))
+
+
+def shard_plan(paths: int, rank: int, world: int) -> dict:
+    L = load_library()
+    s = ShardC()
+    rc = L.ltg_shard_plan(paths, rank, world, C.byref(s))
+    if rc:
+        raise ValueError("shard_plan: bad arguments")
+    return {k: getattr(s, k) for k, _ in ShardC._fields_}
+
+
+def nccl_unique_id() -> bytes:
+    L = load_library()
+    buf = C.create_string_buffer(128)
+    if L.ltg_nccl_unique_id(buf):
+        raise EngineError(L.ltg_last_error(None).decode())
+    return buf.raw
+
+
+class Engine:
+    """A model bound to one GPU: the GPU counterpart of a recorded program
+    (record_heston_program(ModelSpec) for Heston-SLV; the config-4 basket)."""
+
+    def __init__(self, spec, device: int = 0):
+        self.lib = load_library()
+        self.spec = spec
+        self._mm = MarshalledModel(spec)
+        h = C.c_void_p()
+        fn = self.lib.ltg_create_heston if self._mm.kind == 0 else self.lib.ltg_create_basket
+        rc = fn(C.cast(self._mm.ptr, C.c_void_p), device, C.byref(h))
+        if rc:
+            msg = self.lib.ltg_last_error(None).decode()
+            raise (ValueError if rc == LTG_EINVAL else EngineError)(msg)
+        self.h = h
+        self.M = self.lib.ltg_num_params(h)
+        self.m = self.lib.ltg_num_outputs(h)
+        self.N = self.lib.ltg_num_randoms(h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ltg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, rc: int):
+        msg = self.lib.ltg_last_error(self.h).decode()
+        if rc == LTG_EINVAL:
+            raise ValueError(msg)
+        if rc == LTG_ENUMERIC:
+            raise EvalError(msg)
+        raise EngineError(msg)
+
+    @property
+    def rng_exact(self) -> bool:
+        return bool(self.lib.ltg_rng_exact(self.h))
+
+    def pack_params(self) -> np.ndarray:
+        x = np.empty(self.M)
+        self.lib.ltg_pack_params(self.h, _p(x), self.M)
+        return x
+
+    def gradient_of_G(self, x, targets, cfg: MCConfig, std_errors: bool = False) -> GradientReport:
+        """expectation.hpp:346-351"""
+        xa, ta = _arr(x), _arr(targets)
+        means, lam, grad = np.empty(self.m), np.empty(self.m), np.empty(self.M)
+        se = np.empty(self.m) if std_errors else None
+        rep = ReportC(0.0, _p(means), _p(lam), _p(grad), _p(se), 0, 0, 0)
+        c = _cfg(cfg)
+        rc = self.lib.ltg_gradient_of_G(self.h, _p(xa), xa.size, _p(ta), ta.size, C.byref(c),
+                                        C.byref(rep))
+        if rc:
+            self._raise(rc)
+        out = GradientReport(rep.G, means.tolist(), lam.tolist(), grad.tolist(), int(rep.paths),
+                             memory_mode_name(rep.mode), int(rep.seed))
+        if std_errors:
+            out.std_errors = se.tolist()
+        return out
+
+    def estimate_means(self, x, cfg: MCConfig) -> MeansResult:
+        """expectation.hpp:281-286"""
+        xa = _arr(x)
+        means, se = np.empty(self.m), np.empty(self.m)
+        c = _cfg(cfg)
+        rc = self.lib.ltg_estimate_means(self.h, _p(xa), xa.size, C.byref(c), _p(means), _p(se))
+        if rc:
+            self._raise(rc)
+        return MeansResult(means.tolist(), se.tolist(), int(cfg.paths))
+
+    def finite_diff_gradient_of_G(self, x, targets, cfg: MCConfig, h: float) -> np.ndarray:
+        """expectation.hpp:372-400"""
+        xa, ta = _arr(x), _arr(targets)
+        g = np.empty(self.M)
+        c = _cfg(cfg)
+        rc = self.lib.ltg_finite_diff_gradient_of_G(self.h, _p(xa), xa.size, _p(ta), ta.size,
+                                                    C.byref(c), h, _p(g))
+        if rc:
+            self._raise(rc)
+        return g
+
+    def fill_normals(self, seed: int, dim: int, antithetic: bool, path0: int,
+                     npaths: int) -> np.ndarray:
+        """PhiloxNormalSource(seed, dim, antithetic).fill(p) for p in [path0, path0+npaths)."""
+        out = np.empty((npaths, dim))
+        rc = self.lib.ltg_fill_normals(self.h, seed, dim, int(antithetic), path0, npaths, _p(out))
+        if rc:
+            self._raise(rc)
+        return out
+
+    def timing(self) -> dict:
+        t = TimingC()
+        self.lib.ltg_last_timing(self.h, C.byref(t))
+        return {k: getattr(t, k) for k, _ in TimingC._fields_}
+
+    def attach_nccl(self, uid: bytes, rank: int, world: int) -> None:
+        rc = self.lib.ltg_attach_nccl(self.h, uid, rank, world)
+        if rc:
+            self._raise(rc)
+
+    # ---- calibrate.hpp:117-120 plug point ----
+    def objective(self, targets, cfg: MCConfig):
+        """(value_and_grad, value) callbacks for the reference's gradient_descent
+        under common random numbers (every call replays cfg.seed)."""
+        ta = list(targets)
+
+        def value_and_grad(x):
+            return self.gradient_of_G(x, ta, cfg)
+
+        def value(x):
+            means = self.estimate_means(x, cfg).means
+            g = 0.0
+            for mv, t in zip(means, ta):
+                l = mv - t
+                g += 0.5 * l * l
+            return g
+
+        return value_and_grad, value

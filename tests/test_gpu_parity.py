@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the CPU oracle.
+
+The oracle is the reference library itself compiled in place
+(oracle/_ref/libltref.so) — its gradient_of_G / estimate_means /
+PhiloxNormalSource — on the same seeded inputs. Bars (north_star,
+BASELINE.json):
+  * random draws: bit-exact;
+  * E[y], lambda, G, grad: relative error <= 1e-10 in fp64 with the
+    denominator max(|a|, |b|, floor), floor = 1e-12 * max|vector|
+    (tests/support/oracles.hpp:19-22 style rel_err).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1901_04200_b200 import configs
+from paper_1901_04200_b200.engine import Engine, EvalError
+from paper_1901_04200_b200.model import MCConfig, MODE_STORE, load_model_spec
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def rel_err(a, b, floor_frac=1e-12):
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    floor = floor_frac * max(np.max(np.abs(a)), np.max(np.abs(b)), 1e-300)
+    return np.max(np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor))
+
+
+def assert_report_close(rep, orc, tol=TOL):
+    assert rel_err(rep.means, orc["means"]) <= tol, (rep.means, orc["means"])
+    assert rel_err(rep.lambda_, orc["lambda_"]) <= tol
+    assert rel_err([rep.G], [orc["G"]]) <= tol, (rep.G, orc["G"])
+    assert rel_err(rep.grad, orc["grad"]) <= tol, (np.asarray(rep.grad), orc["grad"])
+
+
+@pytest.fixture(scope="module")
+def small(golden_dir):
+    spec = load_model_spec(f"{golden_dir}/heston_small.json")
+    return spec, Engine(spec)
+
+
+# ---------------------------------------------------------------- RNG ----
+
+@pytest.mark.parametrize("seed,dim,anti,path0", [
+    (42, 8, False, 7),                   # test_rng.cpp:67-74 hand-derived draws
+    (20190114, 1512, False, 0),          # config-3 path dimension
+    (9001, 6, False, 123456789),
+    (5, 3, False, 0),                    # odd dimension (rng.hpp:124)
+    (77, 4, True, 0),                    # antithetic pairing (rng.hpp:114-115)
+    (31415, 33, True, (1 << 40) + 3),    # high path word, odd dim, antithetic
+    ((1 << 63) + 12345, 128, False, (1 << 33) + 17),
+])
+def test_normals_bit_exact(ref, small, seed, dim, anti, path0):
+    eng = small[1]
+    npaths = 300
+    g = eng.fill_normals(seed, dim, anti, path0, npaths)
+    r = ref.fill_normals(seed, dim, anti, path0, npaths)
+    mism = int(np.sum(g.view(np.uint64) != r.view(np.uint64)))
+    assert mism == 0, f"{mism} of {g.size} draws differ"
+
+
+def test_hand_derived_draws(small):
+    z = small[1].fill_normals(42, 8, False, 7, 1)[0]
+    assert z[6] == 0.020415871554285415
+    assert z[7] == -0.17620946540988347
+
+
+def test_rng_uses_validated_libm_log(small):
+    assert small[1].rng_exact
+
+
+def test_normals_bulk_tail_exact(ref, small):
+    # 2^16 paths x 64 draws: ~630k tail draws through the glibc-log restatement
+    g = small[1].fill_normals(2718, 64, False, 1 << 20, 1 << 16)
+    r = ref.fill_normals(2718, 64, False, 1 << 20, 1 << 16)
+    assert np.array_equal(g.view(np.uint64), r.view(np.uint64))
+
+
+# ------------------------------------------------------ two-pass gradient ----
+
+def _targets_from(ref_prog, x, paths, seed, scale=0.9):
+    means, _ = ref_prog.estimate_means(x, paths, seed, workers=8)
+    return scale * means
+
+
+@pytest.mark.parametrize("paths", [64, 1000, 4096 + 37])
+def test_heston_small_gradient(ref, small, paths):
+    spec, eng = small
+    prog = ref.program(spec)
+    x = prog.initial_params()
+    targets = _targets_from(prog, x, paths, spec.mc.seed)
+    orc = prog.gradient_of_G(x, targets, paths, spec.mc.seed, workers=8)
+    rep = eng.gradient_of_G(x, targets, MCConfig(paths=paths, seed=spec.mc.seed))
+    assert_report_close(rep, orc)
+
+
+@pytest.mark.parametrize("name,paths", [("cfg1", 1 << 16), ("cfg2", 1 << 14), ("cfg3", 1 << 12),
+                                        ("cfg3", 3000)])
+def test_baseline_configs_gradient(ref, name, paths):
+    c = configs.ALL[name]()
+    eng = Engine(c.spec)
+    prog = ref.program(c.spec)
+    targets = c.targets if c.targets is not None else _targets_from(prog, c.truth, paths, 4242)
+    orc = prog.gradient_of_G(c.x, targets, paths, c.seed, workers=8)
+    rep = eng.gradient_of_G(c.x, targets, MCConfig(paths=paths, seed=c.seed))
+    assert_report_close(rep, orc)
+
+
+def test_estimate_means_and_std_errors(ref, small):
+    spec, eng = small
+    prog = ref.program(spec)
+    x = prog.initial_params()
+    means, se = prog.estimate_means(x, 5000, 99, workers=8)
+    r = eng.estimate_means(x, MCConfig(paths=5000, seed=99))
+    assert rel_err(r.means, means) <= TOL
+    assert rel_err(r.std_errors, se) <= 1e-8  # sqrt of a cancelling difference
+
+
+def test_antithetic(ref, small):
+    spec, eng = small
+    prog = ref.program(spec)
+    x = prog.initial_params()
+    t = _targets_from(prog, x, 2048, 5)
+    orc = prog.gradient_of_G(x, t, 2048 + 1, 5, antithetic=True, workers=8)
+    rep = eng.gradient_of_G(x, t, MCConfig(paths=2048 + 1, seed=5, antithetic=True))
+    assert_report_close(rep, orc)
+
+
+def test_fresh_step2_paths(ref, small):
+    spec, eng = small
+    prog = ref.program(spec)
+    x = prog.initial_params()
+    t = _targets_from(prog, x, 3000, 11)
+    orc = prog.gradient_of_G(x, t, 3000, 11, fresh=True, workers=8)
+    rep = eng.gradient_of_G(x, t, MCConfig(paths=3000, seed=11, fresh_step2_paths=True))
+    assert_report_close(rep, orc)
+
+
+def test_lambda_zero_identity(small):
+    # test_calibrate.cpp:201-221: targets = means at the truth, same seed
+    spec, eng = small
+    x = eng.pack_params()
+    cfg = MCConfig(paths=5000, seed=17)
+    t = eng.estimate_means(x, cfg).means
+    rep = eng.gradient_of_G(x, t, cfg)
+    assert rep.G == 0.0
+    assert all(v == 0.0 for v in rep.lambda_)
+    assert all(v == 0.0 for v in rep.grad)
+
+
+def test_rerun_bitwise_deterministic(small):
+    spec, eng = small
+    x = eng.pack_params()
+    cfg = MCConfig(paths=70001, seed=3)
+    t = [v * 0.9 for v in eng.estimate_means(x, cfg).means]
+    a = eng.gradient_of_G(x, t, cfg)
+    b = eng.gradient_of_G(x, t, cfg)
+    assert a.to_json() == b.to_json()
+
+
+def test_gpu_fd_matches_adjoint(small):
+    # acceptance.cpp:125-154 criterion 1 on the GPU: central differences of G
+    # under common random numbers vs the two-pass gradient, 1e-6
+    spec, eng = small
+    x = eng.pack_params()
+    cfg = MCConfig(paths=spec.mc.paths, seed=spec.mc.seed)
+    t = [0.9 * v for v in eng.estimate_means(x, cfg).means]
+    rep = eng.gradient_of_G(x, t, cfg)
+    fd = eng.finite_diff_gradient_of_G(x, t, cfg, 3e-7)
+    g = np.asarray(rep.grad)
+    assert np.max(np.abs(g - fd) / np.maximum(np.abs(g), 1e-8)) <= 1e-6
+
+
+def test_report_fields_and_json(small):
+    spec, eng = small
+    x = eng.pack_params()
+    rep = eng.gradient_of_G(x, [1.0] * 4, MCConfig(paths=100, seed=8, memory_mode=MODE_STORE))
+    assert rep.paths == 100 and rep.seed == 8 and rep.mode == "store"
+    assert list(__import__("json").loads(rep.to_json()).keys()) == \
+        ["G", "means", "lambda", "grad", "paths", "mode", "seed"]
+
+
+def test_error_behaviour(small):
+    spec, eng = small
+    x = eng.pack_params()
+    with pytest.raises(ValueError):
+        eng.gradient_of_G(x[:-1], [1.0] * 4, MCConfig(paths=10, seed=1))
+    with pytest.raises(ValueError):
+        eng.gradient_of_G(x, [1.0] * 3, MCConfig(paths=10, seed=1))
+    with pytest.raises(ValueError):
+        eng.gradient_of_G(x, [1.0] * 4, MCConfig(paths=0, seed=1))
+    with pytest.raises(ValueError):
+        eng.gradient_of_G(x, [1.0] * 4, MCConfig(paths=10, seed=1, memory_mode=MODE_STORE,
+                                                 fresh_step2_paths=True))
+    bad = list(x)
+    bad[3] = 1.5  # rho: sqrt(1 - rho^2) of a negative -> EvalError in the reference
+    with pytest.raises(EvalError):
+        eng.gradient_of_G(bad, [1.0] * 4, MCConfig(paths=10, seed=1))
