@@ -1,0 +1,289 @@
+#!/usr/bin/env python
+"""bench.py — ∇G Monte-Carlo paths/s of the two-pass gradient (BASELINE.json).
+
+Default workload: BASELINE config 5 — config 3's Heston model and 60-call
+option set (756 full-truncation Euler steps) at P = 2^26 paths, fp64, on N
+GPUs (one process per GPU under torchrun). A "step" is one full
+gradient_of_G call: pass 1 + means/lambda/G + pass 2 + grad, all P paths.
+
+  value  whole-job paths/s from device time (CUDA events the library records
+         on its stream around each call), max over ranks;
+  e2e    the same metric through the C-ABI call with host buffers (x and the
+         targets copied in, the report copied out every step), wall clock
+         bracketed by synchronisation, max over ranks.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libltref.so, the unmodified lanetape headers compiled in place)
+on this host's cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1901_04200_b200 import census, configs  # noqa: E402
+from paper_1901_04200_b200.model import FP32, FP64, MCConfig  # noqa: E402
+
+METRIC = "grad_G_mc_paths_per_sec"
+UNIT = "paths/s"
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rate(cfg, targets, sample_paths, workers, reps=1):
+    """The reference's gradient_of_G (MCConfig{lane_width=8, workers, Recompute}) on a
+    bounded sample; returns (paths/s, seconds)."""
+    from oracle.bindings import Ref
+    prog = Ref().program(cfg.spec)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        prog.gradient_of_G(cfg.x, targets, sample_paths, cfg.seed, lane_width=8, workers=workers)
+        dt = time.perf_counter() - t0
+        best = dt if best is None or dt < best else best
+    return sample_paths / best, best
+
+
+def size_cpu_sample(cfg, targets, workers, seconds):
+    probe = 1024
+    rate, _ = cpu_reference_rate(cfg, targets, probe, workers)
+    return max(probe, int(rate * seconds) // 1024 * 1024), rate
+
+
+def build_cfg(name, paths):
+    c = configs.ALL[name]() if name != "cfg5" else configs.cfg5()
+    if paths:
+        c.paths = paths
+        if hasattr(c.spec, "mc"):
+            c.spec.mc.paths = paths
+    return c
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    cfg = build_cfg(args.config, args.paths)
+    targets = configs.load_targets(cfg) or [1.0] * cfg.m
+    workers = os.cpu_count() or 1
+    sample, _ = size_cpu_sample(cfg, targets, workers, args.ref_seconds)
+    for _ in range(args.warmup):
+        cpu_reference_rate(cfg, targets, max(1024, sample // 8), workers)
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_reference_rate(cfg, targets, sample, workers)
+        times.append(dt)
+    value = sample / statistics.mean(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg.name, "paths": cfg.paths,
+                                        "sample_paths_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+                         "sample": f"{sample} of the workload's paths per step, lane_width=8, "
+                                   f"{workers} worker threads, recompute mode"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--config", default="cfg5", choices=sorted(configs.ALL))
+    ap.add_argument("--paths", type=int, default=0, help="override the config's path count")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--ref-seconds", type=float, default=4.0,
+                    help="target time of one --impl reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 0 and args.steps >= 1
+    rank, world, local = dist_env()
+
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group(backend="gloo")
+        pg = dist
+
+    if args.impl == "reference":
+        rc = run_reference(args, rank, world)
+        if pg:
+            pg.barrier()
+            pg.destroy_process_group()
+        return rc
+
+    from paper_1901_04200_b200.engine import Engine, nccl_unique_id, probe_fp64_rate
+
+    cfg = build_cfg(args.config, args.paths)
+    targets = configs.load_targets(cfg)
+    if targets is None:
+        # separate-seed forward run at the truth (synthetic_targets, calibrate.hpp:224-227)
+        e0 = Engine(cfg.spec, device=local)
+        targets = e0.estimate_means(cfg.truth, MCConfig(paths=configs.TARGET_PATHS,
+                                                        seed=configs.TARGET_SEED)).means
+        e0.close()
+    eng = Engine(cfg.spec, device=local)
+    if world > 1:
+        import torch
+        obj = [nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(obj, src=0)
+        eng.attach_nccl(obj[0], rank, world)
+    mc = MCConfig(paths=cfg.paths, seed=cfg.seed,
+                  precision=FP32 if args.precision == "fp32" else FP64)
+
+    for _ in range(args.warmup):
+        eng.gradient_of_G(cfg.x, targets, mc)
+
+    # ---- timed region: K full gradient_of_G calls ----
+    if pg:
+        pg.barrier()
+    dev_ms, p1_ms, p2_ms, launches = [], [], [], 0
+    with Clocks(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rep = eng.gradient_of_G(cfg.x, targets, mc)   # host buffers in, report out, synced
+            tm = eng.timing()
+            dev_ms.append(tm["total_ms"])
+            p1_ms.append(tm["pass1_ms"])
+            p2_ms.append(tm["pass2_ms"])
+            launches += tm["launches"]
+        wall = time.perf_counter() - t0
+    clocks = clk.summary()
+    dev_total = sum(dev_ms)
+    if pg:
+        import torch
+        t = torch.tensor([dev_total, wall, sum(p2_ms), sum(p1_ms)], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        dev_total, wall, p2_tot, p1_tot = t.tolist()
+    else:
+        p2_tot, p1_tot = sum(p2_ms), sum(p1_ms)
+
+    out = None
+    if rank == 0:
+        K = args.steps
+        value = cfg.paths * K / (dev_total * 1e-3)
+        e2e = cfg.paths * K / wall
+        peak = probe_fp64_rate(local)
+        w2 = census.pass2_fp64_per_path(cfg.name, args.precision)
+        paths_rank = tm["paths_pass2"]
+        achieved = (w2 * paths_rank / (p2_tot / K * 1e-3)) if w2 else None
+        roof = {"bound": "fp64", "kernel": "heston_pass2_kernel",
+                "achieved": achieved / 1e12 if achieved else None,
+                "peak": peak / 1e12, "unit": "T fp64-inst/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "census_fp64_per_path": w2,
+                "peak_source": "measured in this run: ltg_probe_fp64_rate (DFMA, 8 chains/thread)"}
+        trf = census.pass2_dram_bytes_per_path(cfg.name, args.precision)
+        if trf is not None:
+            roof["traffic"] = trf * paths_rank
+        M, m = len(cfg.x), cfg.m
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": dev_total / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.precision == "fp64" else "f32",
+            "data": "synthetic (seeded Philox paths; no dataset)",
+            "config": {"workload": cfg.name, "model": cfg.description, "paths": cfg.paths,
+                       "seed": cfg.seed, "parallelism": f"path-sharded dp{world}",
+                       "l2": "working set > L2: HBM checkpoint table "
+                             f"{census.ckpt_bytes(cfg)/1e9:.1f} GB rewritten every step"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * (M + m),
+                    "d2h_bytes_per_step": 8 * (1 + 3 * m + M)},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "roofline": roof,
+            "pass_ms": {"pass1": p1_tot / K, "pass2": p2_tot / K},
+            "G": rep.G,
+            "rng_exact": eng.rng_exact,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            workers = os.cpu_count() or 1
+            try:
+                sample, _ = size_cpu_sample(cfg, targets, workers, args.cpu_seconds)
+                rate, secs = cpu_reference_rate(cfg, targets, sample, workers)
+                line["cpu_baseline"] = {
+                    "value": rate, "unit": UNIT, "cores": workers, "kind": "reference",
+                    "sample": f"{sample} paths of {cfg.name} through the reference's "
+                              f"gradient_of_G (lane_width=8, recompute), {secs:.1f} s"}
+            except Exception as e:  # the oracle is optional on the box
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": workers,
+                                        "kind": "reference", "sample": f"unavailable: {e}"}
+        out = line
+        print(json.dumps(out), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

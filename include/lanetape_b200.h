@@ -199,6 +199,18 @@ int ltg_shard_plan(uint64_t paths, int rank, int world, ltg_shard* out);
 int ltg_nccl_unique_id(unsigned char id[128]);
 int ltg_attach_nccl(ltg_ctx* ctx, const unsigned char id[128], int rank, int world);
 
+/* Diagnostic: measured FP64 DFMA issue rate of `device` (thread-DFMAs per
+ * second, 8 independent chains per thread, best of 5) — the roofline
+ * denominator reported by bench.py. */
+int ltg_probe_fp64_rate(int device, double* dfma_per_s, double* sm_clock_hz);
+
+/* Host-only self-test of the random stream's log(): locates and validates
+ * the host libm table (as context creation does) and compares the GPU's
+ * restated log sequence, evaluated on the host, with log() on n tail
+ * arguments. Returns 0 when a table was found; *mismatches counts
+ * disagreements (expected 0), *exact is what ltg_rng_exact would report. */
+int ltg_rng_selftest(uint64_t n, uint64_t* mismatches, int* exact);
+
 #ifdef __cplusplus
 }
 #endif

@@ -128,6 +128,7 @@ uint64_t chunks_per_rank(const ltg_shard& s, int world) {
 
 struct ltg_ctx {
     int kind = 0;  // 0 Heston SLV, 1 basket
+    bool ready = false;  // device state initialised
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[8] = {};
@@ -181,7 +182,7 @@ namespace {
 template <typename Fn>
 int guarded(ltg_ctx* ctx, Fn&& fn) {
     try {
-        if (ctx) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (ctx && ctx->ready) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         fn();
         return LTG_OK;
     } catch (const Failure& f) {
@@ -225,6 +226,7 @@ void init_common(ltg_ctx* c, int device) {
     cuda_check(cudaMemcpy(c->d_rng.p, &c->h_rng, sizeof(RngTables), cudaMemcpyHostToDevice),
                "rng upload");
     c->d_counter.ensure(64 * sizeof(uint32_t));
+    c->ready = true;
 }
 
 // maturity events from instrument maturity steps (stable order, like the

@@ -41,6 +41,8 @@ uint64_t d2bits(double d) {
     return u;
 }
 
+}  // namespace
+
 // host restatement of rng.cuh:glibc_log (std::fma == __fma_rn bit for bit)
 double emulate_log(const RngTables& t, double x) {
     const uint64_t ix = d2bits(x);
@@ -66,6 +68,8 @@ double emulate_log(const RngTables& t, double x) {
     volatile double out = y + hi;
     return out;
 }
+
+namespace {
 
 bool read_file(const char* path, std::vector<unsigned char>& buf) {
     std::ifstream f(path, std::ios::binary);
@@ -175,3 +179,26 @@ void fill_as241(RngTables& t) {
 }
 
 }  // namespace ltg
+
+// Host-only self-test behind ltg_rng_selftest: discovers the table and
+// compares the restated log against the host log() on n pseudo-random tail
+// arguments (2n+1)*2^-53 folded into (0, 0.075].
+extern "C" int ltg_rng_selftest(uint64_t n, uint64_t* mismatches, int* exact) {
+    ltg::RngTables t{};
+    std::string why;
+    const bool ok = ltg::discover_glibc_log(t, why);
+    if (exact) *exact = ok ? 1 : 0;
+    uint64_t bad = 0, s = 0x243F6A8885A308D3ULL;
+    for (uint64_t i = 0; i < n && ok; ++i) {
+        s ^= s << 13;
+        s ^= s >> 7;
+        s ^= s << 17;
+        const uint64_t k = s >> 12;
+        double x = ((double)(2 * k + 1)) * 0x1p-53;
+        if (x > 0.5) x = 1.0 - x;
+        if (x > 0.075) x *= 0.075;
+        if (ltg::emulate_log(t, x) != std::log(x)) ++bad;
+    }
+    if (mismatches) *mismatches = bad;
+    return ok ? 0 : 1;
+}

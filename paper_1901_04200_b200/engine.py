@@ -66,8 +66,27 @@ def load_library(path: str = LIB_PATH):
     L.ltg_shard_plan.argtypes = [C.c_uint64, C.c_int, C.c_int, C.POINTER(ShardC)]
     L.ltg_nccl_unique_id.argtypes = [C.c_char_p]
     L.ltg_attach_nccl.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int]
+    L.ltg_probe_fp64_rate.argtypes = [C.c_int, _dp, _dp]
+    L.ltg_rng_selftest.argtypes = [C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]
     _lib = L
     return L
+
+
+def probe_fp64_rate(device: int = 0) -> float:
+    """Measured DFMA issue rate (thread-DFMAs/s) of the GPU."""
+    L = load_library()
+    r, clk = C.c_double(), C.c_double()
+    if L.ltg_probe_fp64_rate(device, C.byref(r), C.byref(clk)):
+        raise EngineError("fp64 probe failed")
+    return r.value
+
+
+def rng_selftest(n: int = 1 << 20):
+    """Host-only check of the GPU log restatement against this host's libm."""
+    L = load_library()
+    bad, exact = C.c_uint64(), C.c_int()
+    rc = L.ltg_rng_selftest(n, C.byref(bad), C.byref(exact))
+    return {"found": rc == 0, "mismatches": bad.value, "exact": bool(exact.value)}
 
 
 def _arr(x: Sequence[float]) -> np.ndarray:
