@@ -28,8 +28,8 @@
 #include "kernels.h"
 
 namespace ltg {
-bool discover_glibc_log(RngTables& t, std::string& why);
-void fill_as241(RngTables& t);
+std::string discover_glibc_math(RngConsts& K, RngTables& T);
+void fill_as241(RngConsts& K);
 }  // namespace ltg
 
 using namespace ltg;
@@ -139,12 +139,15 @@ struct ltg_ctx {
     uint32_t steps = 0, cols = 1, rows = 1, nlev = 1, m = 0, M = 0, N = 0;
     double s0 = 0, mu = 0, dt = 0;
     std::vector<double> x0;
+    std::vector<double> h_x;  // parameters of the current call
     std::vector<MaturityEvent> events;
     std::vector<uint32_t> inst_order;
 
     // model (device)
-    DevBuf d_snodes, d_rowoff, d_events, d_order, d_strike, d_kind, d_rng;
-    RngTables h_rng{};
+    DevBuf d_snodes, d_rowoff, d_events, d_order, d_strike, d_kind, d_tab;
+    RngConsts h_rc{};
+    RngTables h_tab{};
+    uint32_t seg_steps = 16;  // checkpoint interval of the current call
 
     // per-call buffers
     DevBuf d_x, d_targets, d_part1, d_part2, d_groups, d_tot1, d_tot2, d_res, d_grad, d_counter,
@@ -219,11 +222,10 @@ void init_common(ltg_ctx* c, int device) {
                                      " is not sm_100 (this library is built for sm_100a only)");
     cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     for (auto& e : c->ev) cuda_check(cudaEventCreate(&e), "event");
-    fill_as241(c->h_rng);
-    std::string why;
-    if (!discover_glibc_log(c->h_rng, why)) c->rng_note = why;
-    c->d_rng.ensure(sizeof(RngTables));
-    cuda_check(cudaMemcpy(c->d_rng.p, &c->h_rng, sizeof(RngTables), cudaMemcpyHostToDevice),
+    fill_as241(c->h_rc);
+    c->rng_note = discover_glibc_math(c->h_rc, c->h_tab);
+    c->d_tab.ensure(sizeof(RngTables));
+    cuda_check(cudaMemcpy(c->d_tab.p, &c->h_tab, sizeof(RngTables), cudaMemcpyHostToDevice),
                "rng upload");
     c->d_counter.ensure(64 * sizeof(uint32_t));
     c->ready = true;
@@ -267,7 +269,7 @@ struct Pass1Out {
     bool have_ckpt = false;
 };
 
-HestonArgs heston_args(ltg_ctx* c) {
+HestonArgs heston_args(ltg_ctx* c, const double* x) {
     HestonArgs a{};
     a.steps = c->steps;
     a.cols = c->cols;
@@ -280,6 +282,23 @@ HestonArgs heston_args(ltg_ctx* c) {
     a.sqdt = std::sqrt(c->dt);
     a.mu_dt = c->mu * c->dt;
     a.half_dt = 0.5 * c->dt;
+    // step constants, rounded exactly as the reference tape computes them
+    a.sc.kappa = x[0];
+    a.sc.theta = x[1];
+    a.sc.xi = x[2];
+    a.sc.rho = x[3];
+    {
+        volatile double rr = x[3] * x[3];
+        volatile double u = 1.0 - rr;
+        volatile double su = std::sqrt((double)u);
+        volatile double sq = std::sqrt(c->dt);
+        a.sc.rc = su * sq;
+        a.sqdt = sq;
+    }
+    a.sc.dt = c->dt;
+    a.sc.sqdt = a.sqdt;
+    a.sc.mu_dt = a.mu_dt;
+    a.sc.half_dt = a.half_dt;
     a.x = c->d_x.as<double>();
     a.s_nodes = c->d_snodes.as<double>();
     a.row_off = c->d_rowoff.as<uint16_t>();
@@ -287,7 +306,9 @@ HestonArgs heston_args(ltg_ctx* c) {
     a.inst_order = c->d_order.as<uint32_t>();
     a.strike = c->d_strike.as<double>();
     a.kind = c->d_kind.as<int32_t>();
-    a.rng = c->d_rng.as<RngTables>();
+    a.tables = c->d_tab.as<RngTables>();
+    a.rc = c->h_rc;
+    a.seg_steps = c->seg_steps;
     return a;
 }
 
@@ -341,19 +362,36 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     c->d_tot1.ensure(width * 8);
     c->d_res.ensure((1 + 3 * c->m) * 8);
 
-    HestonArgs a = heston_args(c);
     Work w = base_work(c, cfg, plan);
-    const uint32_t nseg = (c->steps + kSegSteps - 1) / kSegSteps;
+    // checkpoint interval: 8 steps (more resident CTAs in pass 2) when the
+    // table fits in HBM next to a 2 GiB reserve, else 16, else no table
+    // (pass 2 then replays its checkpoints in waves)
     bool ckpt = false;
-    if (want_ckpt && nseg > 1) {
-        const size_t need = size_t(nseg - 1) * w.ckpt_stride * 16;
+    c->seg_steps = 16;
+    if (want_ckpt) {
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
-        if (need <= c->d_ckpt.bytes || need + (size_t(2) << 30) < free_b) {
-            c->d_ckpt.ensure(need);
-            ckpt = true;
+        const size_t avail = free_b + c->d_ckpt.bytes > (size_t(2) << 30)
+                                 ? free_b + c->d_ckpt.bytes - (size_t(2) << 30)
+                                 : 0;
+        for (uint32_t ks : {8u, 16u}) {
+            const uint32_t nseg = (c->steps + ks - 1) / ks;
+            const size_t need = size_t(nseg > 1 ? nseg - 1 : 0) * w.ckpt_stride * 16;
+            if (need <= avail) {
+                c->seg_steps = ks;
+                if (need > c->d_ckpt.bytes) {
+                    c->d_ckpt.ensure(0);
+                    if (c->d_ckpt.p) cudaFree(c->d_ckpt.p);
+                    c->d_ckpt.p = nullptr;
+                    c->d_ckpt.bytes = 0;
+                    c->d_ckpt.ensure(need);
+                }
+                ckpt = nseg > 1;
+                break;
+            }
         }
     }
+    HestonArgs a = heston_args(c, c->h_x.data());
     a.partials = c->d_part1.as<double>() + plan.chunk_begin * width;
     a.ckpt = ckpt ? c->d_ckpt.as<double2>() : nullptr;
     a.write_sums = 1;
@@ -384,10 +422,10 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     c->d_part2.ensure(table_rows * c->M * 8);
     c->d_tot2.ensure(c->M * 8);
     c->d_grad.ensure(c->M * 8);
-    HestonArgs a = heston_args(c);
+    HestonArgs a = heston_args(c, c->h_x.data());
     a.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
     Work w = base_work(c, cfg, plan);
-    const uint32_t nseg = (c->steps + kSegSteps - 1) / kSegSteps;
+    const uint32_t nseg = (c->steps + c->seg_steps - 1) / c->seg_steps;
     cuda_check(cudaEventRecord(c->ev[3], c->stream), "event");
     if (w.n_chunks) {
         if (!have_ckpt && nseg > 1) {
@@ -456,6 +494,7 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 }
 
 void upload_x(ltg_ctx* c, const double* x, const double* targets) {
+    c->h_x.assign(x, x + c->M);
     const size_t n = c->M + (targets ? c->m : 0);
     double* st = c->stage(n);
     std::memcpy(st, x, c->M * 8);
@@ -580,7 +619,9 @@ int ltg_pack_params(const ltg_ctx* ctx, double* x, size_t M) {
     return LTG_OK;
 }
 
-int ltg_rng_exact(const ltg_ctx* ctx) { return ctx ? ctx->h_rng.exact : 0; }
+int ltg_rng_exact(const ltg_ctx* ctx) {
+    return ctx ? (ctx->h_rc.exact_log && ctx->h_rc.exact_exp) : 0;
+}
 
 int ltg_shard_plan(uint64_t paths, int rank, int world, ltg_shard* out) {
     if (!out || world < 1 || rank < 0 || rank >= world || paths == 0) return LTG_EINVAL;
@@ -709,7 +750,7 @@ int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, ui
         const size_t n = size_t(npaths) * dim;
         if (n == 0) return;
         ctx->d_normals.ensure(n * 8);
-        cuda_check(launch_fill_normals(ctx->d_rng.as<RngTables>(), (uint32_t)seed,
+        cuda_check(launch_fill_normals(ctx->d_tab.as<RngTables>(), ctx->h_rc, (uint32_t)seed,
                                        (uint32_t)(seed >> 32), antithetic, path0, npaths,
                                        (uint32_t)dim, ctx->d_normals.as<double>(), ctx->stream),
                    "fill_normals");
@@ -717,6 +758,41 @@ int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, ui
                                    ctx->stream),
                    "D2H");
         cuda_check(cudaStreamSynchronize(ctx->stream), "fill_normals");
+    });
+}
+
+int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int antithetic,
+                     uint64_t path0, uint64_t npaths, double* y) {
+    if (!ctx) return LTG_EINVAL;
+    return guarded(ctx, [&] {
+        require(x && y && M == ctx->M, "path_payoffs: size mismatch");
+        require(ctx->kind == 0, "path_payoffs: Heston-SLV programs only");
+        check_params(ctx, x);
+        if (npaths == 0) return;
+        upload_x(ctx, x, nullptr);
+        ltg_mc_config cfg{npaths, seed, antithetic, 0, 0, LTG_FP64};
+        ltg_shard plan{};
+        plan.chunk_paths = kBlock;
+        plan.n_chunks = (npaths + kBlock - 1) / kBlock;
+        plan.chunk_begin = 0;
+        plan.chunk_end = plan.n_chunks;
+        Work w = base_work(ctx, cfg, plan);
+        w.path_offset = path0;
+        w.ckpt_path0 = 0;
+        ctx->seg_steps = 16;
+        HestonArgs a = heston_args(ctx, ctx->h_x.data());
+        ctx->d_part1.ensure(plan.n_chunks * 2 * ctx->m * 8);
+        ctx->d_normals.ensure(npaths * ctx->m * 8);
+        a.partials = ctx->d_part1.as<double>();
+        a.path_out = ctx->d_normals.as<double>();
+        a.write_sums = 1;
+        a.write_ckpt = 0;
+        zero_counter(ctx, 0);
+        cuda_check(launch_heston_pass1(a, w, 0, ctx->stream), "path payoffs");
+        cuda_check(cudaMemcpyAsync(y, ctx->d_normals.p, npaths * ctx->m * 8,
+                                   cudaMemcpyDeviceToHost, ctx->stream),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "path payoffs");
     });
 }
 

@@ -78,26 +78,29 @@ __global__ void finalize_grad_kernel(const double* __restrict__ totals, uint32_t
 
 // PhiloxNormalSource::fill for a path range through the production
 // generator (gen_segment), one path per thread.
-constexpr int KS = kSegSteps;
+constexpr int KF = 16;
 __global__ void __launch_bounds__(kBlock) fill_normals_kernel(
-    const RngTables* rng, uint32_t seed_lo, uint32_t seed_hi, int antithetic, uint64_t path0,
-    uint64_t npaths, uint32_t dim, double* __restrict__ out) {
+    const RngTables* tables, RngConsts rc, uint32_t seed_lo, uint32_t seed_hi, int antithetic,
+    uint64_t path0, uint64_t npaths, uint32_t dim, double* __restrict__ out) {
     __shared__ RngTables sh;
-    __shared__ double zbuf[2 * KS * kBlock];
-    load_rng_shared(&sh, rng);
+    __shared__ double zbuf[2 * KF * kBlock];
+    __shared__ uint16_t wlist[kWarps * 64 * KF];
+    load_tables(&sh, tables);
     __syncthreads();
     const uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
     const uint64_t path = path0 + (i < npaths ? i : npaths - 1);
     const uint64_t base = antithetic ? path >> 1 : path;
     const bool neg = antithetic && (path & 1u);
     const uint32_t pairs = (dim + 1) / 2;
-    for (uint32_t k0 = 0; k0 < pairs; k0 += KS) {
-        const int kn = (int)min((uint32_t)KS, pairs - k0);
-        gen_segment<KS>(base, neg, k0, kn, seed_lo, seed_hi, zbuf, sh);
+    double* zb = zbuf + threadIdx.x;
+    uint16_t* wl = wlist + (threadIdx.x >> 5) * 64 * KF;
+    for (uint32_t k0 = 0; k0 < pairs; k0 += KF) {
+        const int kn = (int)min((uint32_t)KF, pairs - k0);
+        gen_segment<KF>(base, neg, k0, kn, seed_lo, seed_hi, zb, wl, sh, rc);
         if (i < npaths)
             for (int s = 0; s < 2 * kn; ++s) {
                 const uint32_t slot = 2 * k0 + s;
-                if (slot < dim) out[i * dim + slot] = zbuf[s * kBlock + threadIdx.x];
+                if (slot < dim) out[i * dim + slot] = zb[s * kBlock];
             }
     }
 }
@@ -126,12 +129,12 @@ cudaError_t launch_finalize_grad(const double* totals, uint32_t M, uint64_t path
     return cudaGetLastError();
 }
 
-cudaError_t launch_fill_normals(const RngTables* rng, uint32_t seed_lo, uint32_t seed_hi,
-                                int antithetic, uint64_t path0, uint64_t npaths, uint32_t dim,
-                                double* out, cudaStream_t s) {
+cudaError_t launch_fill_normals(const RngTables* tables, const RngConsts& rc, uint32_t seed_lo,
+                                uint32_t seed_hi, int antithetic, uint64_t path0, uint64_t npaths,
+                                uint32_t dim, double* out, cudaStream_t s) {
     if (npaths == 0 || dim == 0) return cudaSuccess;
     fill_normals_kernel<<<(unsigned)((npaths + kBlock - 1) / kBlock), kBlock, 0, s>>>(
-        rng, seed_lo, seed_hi, antithetic, path0, npaths, dim, out);
+        tables, rc, seed_lo, seed_hi, antithetic, path0, npaths, dim, out);
     return cudaGetLastError();
 }
 

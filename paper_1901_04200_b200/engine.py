@@ -20,8 +20,8 @@ from .cabi import (LTG_ECUDA, LTG_EINVAL, LTG_ENUMERIC, MarshalledModel, MCConfi
                    ShardC, TimingC)
 from .model import GradientReport, MCConfig, MeansResult, memory_mode_name
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
-                        "liblanetape_b200.so")
+LIB_PATH = os.environ.get("LTG_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "liblanetape_b200.so")
 
 _dp = C.POINTER(C.c_double)
 
@@ -62,6 +62,8 @@ def load_library(path: str = LIB_PATH):
     L.ltg_fill_normals.argtypes = [C.c_void_p, C.c_uint64, C.c_size_t, C.c_int, C.c_uint64,
                                    C.c_uint64, _dp]
     L.ltg_last_timing.argtypes = [C.c_void_p, C.POINTER(TimingC)]
+    L.ltg_path_payoffs.argtypes = [C.c_void_p, _dp, C.c_size_t, C.c_uint64, C.c_int, C.c_uint64,
+                                   C.c_uint64, _dp]
     L.ltg_rng_exact.argtypes = [C.c_void_p]
     L.ltg_shard_plan.argtypes = [C.c_uint64, C.c_int, C.c_int, C.POINTER(ShardC)]
     L.ltg_nccl_unique_id.argtypes = [C.c_char_p]
@@ -212,6 +214,16 @@ class Engine:
         if rc:
             self._raise(rc)
         return out
+
+    def path_payoffs(self, x, seed: int, antithetic: bool, path0: int, npaths: int) -> np.ndarray:
+        """Per-path program outputs for the draws of paths [path0, path0+npaths)."""
+        xa = _arr(x)
+        y = np.empty((npaths, self.m))
+        rc = self.lib.ltg_path_payoffs(self.h, _p(xa), xa.size, seed, int(antithetic), path0,
+                                       npaths, _p(y))
+        if rc:
+            self._raise(rc)
+        return y
 
     def timing(self) -> dict:
         t = TimingC()

@@ -79,6 +79,29 @@ def test_normals_bulk_tail_exact(ref, small):
     assert np.array_equal(g.view(np.uint64), r.view(np.uint64))
 
 
+@pytest.mark.parametrize("name", ["heston_small", "cfg1", "cfg2", "cfg3"])
+def test_per_path_payoffs_bit_exact(ref, golden_dir, name):
+    # the GPU forward replays the reference's tape arithmetic operation for
+    # operation (glibc exp and log included): per-path outputs are identical
+    if name == "heston_small":
+        spec = load_model_spec(f"{golden_dir}/heston_small.json")
+        x = None
+    else:
+        c = configs.ALL[name]()
+        spec, x = c.spec, c.x
+    eng = Engine(spec)
+    prog = ref.program(spec)
+    if x is None:
+        x = prog.initial_params()
+    assert eng.rng_exact
+    n, p0, seed = 200, 12345, 777
+    y = eng.path_payoffs(x, seed, False, p0, n)
+    z = ref.fill_normals(seed, prog.N, False, p0, n)
+    want = np.stack([prog.path_adjoint(x, z[i])[0] for i in range(n)])
+    assert np.array_equal(y.view(np.uint64), want.view(np.uint64)), \
+        f"{int(np.sum(y != want))} of {y.size} payoffs differ"
+
+
 # ------------------------------------------------------ two-pass gradient ----
 
 def _targets_from(ref_prog, x, paths, seed, scale=0.9):
