@@ -1,15 +1,15 @@
 #!/bin/bash
-# Build engine variants with different register budgets into _lib/variants/<name>.so
-# usage: tools/build_variants.sh "5 4" "6 5" ...
+# Build engine variants into _lib/variants/<name>.so
+# usage: tools/build_variants.sh "name P1MINB P2MINB [extra nvcc flags...]" ...
 set -e
 cd "$(dirname "$0")/../paper_1901_04200_b200/csrc"
 OUT=../_lib/variants; mkdir -p $OUT/obj
+make -s -C . >/dev/null
 for v in "$@"; do
-  set -- $v; name=p$1_$2${3:+_$3}
-  extra="-DLTG_P1_MINB=$1 -DLTG_P2_MINB=$2 $4"
+  set -- $v; name=$1; p1=$2; p2=$3; shift 3; extra="$*"
   for f in heston reduce probe; do
-    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -ffp-contract=off -I. -I../../include $extra -c $f.cu -o $OUT/obj/${name}_$f.o
+    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -ffp-contract=off -I. -I../../include -DLTG_P1_MINB=$p1 -DLTG_P2_MINB=$p2 $extra -Xptxas -v -c $f.cu -o $OUT/obj/${name}_$f.o 2> $OUT/obj/${name}_$f.log
   done
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/$name.so $OUT/obj/${name}_heston.o $OUT/obj/${name}_reduce.o $OUT/obj/${name}_probe.o ../_lib/obj/engine.o ../_lib/obj/host_libm.o -ldl
-  echo built $OUT/$name.so
+  echo "built $name: $(grep -h registers $OUT/obj/${name}_heston.log | awk '{print $5}' | tr '\n' ' ') spill: $(grep -h spill $OUT/obj/${name}_heston.log | awk '{s+=$5} END {print s}')"
 done
