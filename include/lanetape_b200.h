@@ -184,7 +184,7 @@ int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, ui
 
 /* Per-path outputs of the program (forward_eval, tape.hpp:276-331, on the
  * draws PhiloxNormalSource(seed).fill(p)) for p in [path0, path0+npaths):
- * y is npaths*m, path-major. Heston-SLV programs only. */
+ * y is npaths*m, path-major. */
 int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int antithetic,
                      uint64_t path0, uint64_t npaths, double* y);
 

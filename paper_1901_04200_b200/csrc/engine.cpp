@@ -143,8 +143,14 @@ struct ltg_ctx {
     std::vector<MaturityEvent> events;
     std::vector<uint32_t> inst_order;
 
+    // basket model (host)
+    uint32_t n_assets = 0;
+    double r = 0;
+    std::vector<double> chol, s0v;
+    bool store_ok = false;  // pass 1 of the current call wrote the basket store
+
     // model (device)
-    DevBuf d_snodes, d_rowoff, d_events, d_order, d_strike, d_kind, d_tab;
+    DevBuf d_snodes, d_rowoff, d_events, d_order, d_strike, d_kind, d_asset, d_tab;
     RngConsts h_rc{};
     RngTables h_tab{};
     uint32_t seg_steps = 16;  // checkpoint interval of the current call
@@ -265,9 +271,36 @@ void all_gather_rows(ltg_ctx* c, double* table, uint64_t per_rank, uint32_t widt
         throw Failure(LTG_ECUDA, std::string("ncclAllGather: ") + nccl().GetErrorString(r));
 }
 
-struct Pass1Out {
-    bool have_ckpt = false;
-};
+// Basket step constants from the parameters, rounded exactly as the recorded
+// program computes them (oracle/ref_driver.cpp record_basket).
+BasketArgs basket_args(ltg_ctx* c, const double* x) {
+    BasketArgs a{};
+    a.n = c->n_assets;
+    a.steps = c->steps;
+    a.m = c->m;
+    a.n_events = (uint32_t)c->events.size();
+    a.dt = c->dt;
+    volatile double sq = std::sqrt(c->dt);
+    a.sqdt = sq;
+    for (uint32_t i = 0; i < a.n; ++i) {
+        for (uint32_t j = 0; j < a.n; ++j) a.chol[i * kMaxAssets + j] = c->chol[i * a.n + j];
+        a.s0[i] = c->s0v[i];
+        a.sigma[i] = x[i];
+        volatile double ss = x[i] * x[i];
+        volatile double hs = 0.5 * ss;
+        volatile double rd = c->r - hs;
+        a.drift[i] = rd * c->dt;
+        a.vol[i] = x[i] * a.sqdt;
+    }
+    a.events = c->d_events.as<MaturityEvent>();
+    a.inst_order = c->d_order.as<uint32_t>();
+    a.asset = c->d_asset.as<uint32_t>();
+    a.strike = c->d_strike.as<double>();
+    a.kind = c->d_kind.as<int32_t>();
+    a.tables = c->d_tab.as<RngTables>();
+    a.rc = c->h_rc;
+    return a;
+}
 
 HestonArgs heston_args(ltg_ctx* c, const double* x) {
     HestonArgs a{};
@@ -363,12 +396,36 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     c->d_res.ensure((1 + 3 * c->m) * 8);
 
     Work w = base_work(c, cfg, plan);
+    if (c->kind == 1) {
+        // basket: (S, W) at every maturity for pass 2 (store mode) when it fits
+        BasketArgs b = basket_args(c, c->h_x.data());
+        c->store_ok = false;
+        if (want_ckpt) {
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            const size_t need = size_t(b.n_events) * b.n * w.ckpt_stride * 16;
+            if (need <= c->d_ckpt.bytes || need + (size_t(2) << 30) < free_b) {
+                c->d_ckpt.ensure(need);
+                c->store_ok = true;
+            }
+        }
+        b.partials = c->d_part1.as<double>() + plan.chunk_begin * width;
+        b.store = c->store_ok ? c->d_ckpt.as<double2>() : nullptr;
+        b.store_stride = w.ckpt_stride;
+        b.write_sums = 1;
+        b.write_store = c->store_ok ? 1 : 0;
+        zero_counter(c, 0);
+        cuda_check(cudaEventRecord(c->ev[0], c->stream), "event");
+        if (w.n_chunks) cuda_check(launch_basket_pass1(b, w, 0, c->stream), "basket pass 1");
+        cuda_check(cudaEventRecord(c->ev[1], c->stream), "event");
+        c->timing.launches += w.n_chunks ? 1 : 0;
+    }
     // checkpoint interval: 8 steps (more resident CTAs in pass 2) when the
     // table fits in HBM next to a 2 GiB reserve, else 16, else no table
     // (pass 2 then replays its checkpoints in waves)
     bool ckpt = false;
     c->seg_steps = 16;
-    if (want_ckpt) {
+    if (want_ckpt && c->kind == 0) {
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
         const size_t avail = free_b + c->d_ckpt.bytes > (size_t(2) << 30)
@@ -391,17 +448,21 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
             }
         }
     }
-    HestonArgs a = heston_args(c, c->h_x.data());
-    a.partials = c->d_part1.as<double>() + plan.chunk_begin * width;
-    a.ckpt = ckpt ? c->d_ckpt.as<double2>() : nullptr;
-    a.write_sums = 1;
-    a.write_ckpt = ckpt ? 1 : 0;
-    // partial rows are indexed from the launch's first chunk
-    zero_counter(c, 0);
-    cuda_check(cudaEventRecord(c->ev[0], c->stream), "event");
-    if (w.n_chunks) cuda_check(launch_heston_pass1(a, w, 0, c->stream), "heston pass 1");
-    cuda_check(cudaEventRecord(c->ev[1], c->stream), "event");
-    c->timing.launches += w.n_chunks ? 1 : 0;
+    if (c->kind == 0) {
+        HestonArgs a = heston_args(c, c->h_x.data());
+        // partial rows are indexed from the launch's first chunk
+        a.partials = c->d_part1.as<double>() + plan.chunk_begin * width;
+        a.ckpt = ckpt ? c->d_ckpt.as<double2>() : nullptr;
+        a.write_sums = 1;
+        a.write_ckpt = ckpt ? 1 : 0;
+        zero_counter(c, 0);
+        cuda_check(cudaEventRecord(c->ev[0], c->stream), "event");
+        if (w.n_chunks) cuda_check(launch_heston_pass1(a, w, 0, c->stream), "heston pass 1");
+        cuda_check(cudaEventRecord(c->ev[1], c->stream), "event");
+        c->timing.launches += w.n_chunks ? 1 : 0;
+    } else {
+        ckpt = c->store_ok;
+    }
     all_gather_rows(c, c->d_part1.as<double>(), per, width);
     cuda_check(launch_reduce_chunks(c->d_part1.as<double>(), plan.n_chunks, width,
                                     c->d_groups.as<double>(), c->d_tot1.as<double>(), c->stream),
@@ -427,7 +488,19 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     Work w = base_work(c, cfg, plan);
     const uint32_t nseg = (c->steps + c->seg_steps - 1) / c->seg_steps;
     cuda_check(cudaEventRecord(c->ev[3], c->stream), "event");
-    if (w.n_chunks) {
+    if (w.n_chunks && c->kind == 1) {
+        BasketArgs b = basket_args(c, c->h_x.data());
+        b.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
+        b.partials = c->d_part2.as<double>() + plan.chunk_begin * c->M;
+        b.use_store = have_ckpt && !cfg.fresh_step2_paths ? 1 : 0;
+        b.store = b.use_store ? c->d_ckpt.as<double2>() : nullptr;
+        b.store_stride = w.ckpt_stride;
+        if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
+        zero_counter(c, 2);
+        w.counter = c->d_counter.as<uint32_t>() + 2;
+        cuda_check(launch_basket_pass2(b, w, 0, c->stream), "basket pass 2");
+        c->timing.launches += 1;
+    } else if (w.n_chunks) {
         if (!have_ckpt && nseg > 1) {
             // fresh_step2_paths or no room for a full checkpoint table: replay
             // the pass-2 path set in waves (checkpoint-only forward, then adjoint)
@@ -596,11 +669,62 @@ int ltg_create_heston(const ltg_heston_model* mdl, int device, ltg_ctx** out) {
 }
 
 int ltg_create_basket(const ltg_basket_model* mdl, int device, ltg_ctx** out) {
-    (void)mdl;
-    (void)device;
-    if (out) *out = nullptr;
-    g_create_error = "basket model not available in this build";
-    return LTG_EINVAL;
+    if (!out || !mdl) {
+        g_create_error = "null argument";
+        return LTG_EINVAL;
+    }
+    *out = nullptr;
+    auto c = std::make_unique<ltg_ctx>();
+    const int rc = guarded(c.get(), [&] {
+        const ltg_basket_model& m = *mdl;
+        require(m.n_assets >= 1 && m.n_assets <= (uint32_t)kMaxAssets,
+                "basket: n_assets must be in [1, 16]");
+        require(m.s0 && m.chol && m.sigma, "basket: null array");
+        require(m.steps > 0, "basket: steps must be > 0");
+        require(m.dt > 0.0, "basket: dt must be > 0");
+        require(std::isfinite(m.r), "basket: r must be finite");
+        require(m.n_instruments > 0 && m.n_instruments <= (uint32_t)kMaxInstruments,
+                "basket: 1..256 instruments");
+        for (uint32_t a = 0; a < m.n_assets; ++a) {
+            require(m.s0[a] > 0.0, "basket: s0 must be > 0");
+            for (uint32_t b = 0; b < m.n_assets; ++b)
+                require(std::isfinite(m.chol[a * m.n_assets + b]) &&
+                            (b <= a || m.chol[a * m.n_assets + b] == 0.0),
+                        "basket: chol must be finite and lower-triangular");
+        }
+        for (uint32_t i = 0; i < m.n_instruments; ++i) {
+            require(m.inst_asset[i] < m.n_assets, "basket: instrument asset out of range");
+            require(m.inst_strike[i] > 0.0, "basket: strike must be > 0");
+            require(m.inst_maturity_step[i] >= 1 && m.inst_maturity_step[i] <= m.steps,
+                    "basket: maturity_step must be in [1, steps]");
+            require(m.inst_kind[i] == LTG_CALL || m.inst_kind[i] == LTG_PUT,
+                    "basket: kind must be call or put");
+        }
+        init_common(c.get(), device);
+        c->kind = 1;
+        c->n_assets = m.n_assets;
+        c->steps = m.steps;
+        c->dt = m.dt;
+        c->r = m.r;
+        c->m = m.n_instruments;
+        c->M = m.n_assets;
+        c->N = m.steps * m.n_assets;
+        c->chol.assign(m.chol, m.chol + m.n_assets * m.n_assets);
+        c->s0v.assign(m.s0, m.s0 + m.n_assets);
+        c->x0.assign(m.sigma, m.sigma + m.n_assets);
+        upload(c->d_strike, std::vector<double>(m.inst_strike, m.inst_strike + m.n_instruments));
+        upload(c->d_kind, std::vector<int32_t>(m.inst_kind, m.inst_kind + m.n_instruments));
+        upload(c->d_asset, std::vector<uint32_t>(m.inst_asset, m.inst_asset + m.n_instruments));
+        build_events(c.get(), std::vector<uint32_t>(m.inst_maturity_step,
+                                                     m.inst_maturity_step + m.n_instruments));
+        cuda_check(cudaDeviceSynchronize(), "init");
+    });
+    if (rc != LTG_OK) {
+        g_create_error = c->err;
+        return rc;
+    }
+    *out = c.release();
+    return LTG_OK;
 }
 
 void ltg_destroy(ltg_ctx* ctx) { delete ctx; }
@@ -766,7 +890,6 @@ int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int
     if (!ctx) return LTG_EINVAL;
     return guarded(ctx, [&] {
         require(x && y && M == ctx->M, "path_payoffs: size mismatch");
-        require(ctx->kind == 0, "path_payoffs: Heston-SLV programs only");
         check_params(ctx, x);
         if (npaths == 0) return;
         upload_x(ctx, x, nullptr);
@@ -780,15 +903,23 @@ int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int
         w.path_offset = path0;
         w.ckpt_path0 = 0;
         ctx->seg_steps = 16;
-        HestonArgs a = heston_args(ctx, ctx->h_x.data());
         ctx->d_part1.ensure(plan.n_chunks * 2 * ctx->m * 8);
         ctx->d_normals.ensure(npaths * ctx->m * 8);
-        a.partials = ctx->d_part1.as<double>();
-        a.path_out = ctx->d_normals.as<double>();
-        a.write_sums = 1;
-        a.write_ckpt = 0;
         zero_counter(ctx, 0);
-        cuda_check(launch_heston_pass1(a, w, 0, ctx->stream), "path payoffs");
+        if (ctx->kind == 0) {
+            HestonArgs a = heston_args(ctx, ctx->h_x.data());
+            a.partials = ctx->d_part1.as<double>();
+            a.path_out = ctx->d_normals.as<double>();
+            a.write_sums = 1;
+            a.write_ckpt = 0;
+            cuda_check(launch_heston_pass1(a, w, 0, ctx->stream), "path payoffs");
+        } else {
+            BasketArgs b = basket_args(ctx, ctx->h_x.data());
+            b.partials = ctx->d_part1.as<double>();
+            b.path_out = ctx->d_normals.as<double>();
+            b.write_sums = 1;
+            cuda_check(launch_basket_pass1(b, w, 0, ctx->stream), "path payoffs");
+        }
         cuda_check(cudaMemcpyAsync(y, ctx->d_normals.p, npaths * ctx->m * 8,
                                    cudaMemcpyDeviceToHost, ctx->stream),
                    "D2H");

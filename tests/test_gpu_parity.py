@@ -79,7 +79,7 @@ def test_normals_bulk_tail_exact(ref, small):
     assert np.array_equal(g.view(np.uint64), r.view(np.uint64))
 
 
-@pytest.mark.parametrize("name", ["heston_small", "cfg1", "cfg2", "cfg3"])
+@pytest.mark.parametrize("name", ["heston_small", "cfg1", "cfg2", "cfg3", "cfg4"])
 def test_per_path_payoffs_bit_exact(ref, golden_dir, name):
     # the GPU forward replays the reference's tape arithmetic operation for
     # operation (glibc exp and log included): per-path outputs are identical
@@ -130,6 +130,45 @@ def test_baseline_configs_gradient(ref, name, paths):
     orc = prog.gradient_of_G(c.x, targets, paths, c.seed, workers=8)
     rep = eng.gradient_of_G(c.x, targets, MCConfig(paths=paths, seed=c.seed))
     assert_report_close(rep, orc)
+
+
+@pytest.mark.parametrize("paths,fresh,anti", [(1 << 12, False, False), (3001, False, False),
+                                              (2048, True, False), (2049, False, True)])
+def test_basket_gradient(ref, paths, fresh, anti):
+    # config 4: 16 correlated GBMs; store mode (pass 1 keeps (S, W) at the
+    # maturity) and, with fresh_step2_paths, recompute mode
+    c = configs.cfg4()
+    eng = Engine(c.spec)
+    prog = ref.program(c.spec)
+    orc = prog.gradient_of_G(c.x, c.targets, paths, c.seed, antithetic=anti, fresh=fresh,
+                             workers=8)
+    rep = eng.gradient_of_G(c.x, c.targets, MCConfig(paths=paths, seed=c.seed,
+                                                      fresh_step2_paths=fresh, antithetic=anti))
+    assert_report_close(rep, orc)
+
+
+def test_basket_multi_maturity_puts(ref):
+    # general maturities, puts and calls, fewer assets
+    import math
+    from paper_1901_04200_b200.model import BasketSpec, Instrument, CALL, PUT
+    n, steps = 5, 12
+    corr = configs.basket_correlation(n, seed=99)
+    L = configs.cholesky(corr)
+    ins, assets = [], []
+    for a in range(n):
+        ins += [Instrument(CALL, 100.0, 4 + a), Instrument(PUT, 98.0, steps)]
+        assets += [a, a]
+    spec = BasketSpec([100.0 + a for a in range(n)], 0.03, [L[i][j] for i in range(n)
+                                                             for j in range(n)],
+                      [0.2] * n, ins, assets, steps, 1.0 / 12)
+    x = [0.15 + 0.05 * a for a in range(n)]
+    eng = Engine(spec)
+    prog = ref.program(spec)
+    t = [1.0] * len(ins)
+    for fresh in (False, True):
+        orc = prog.gradient_of_G(x, t, 4099, 9, fresh=fresh, workers=8)
+        rep = eng.gradient_of_G(x, t, MCConfig(paths=4099, seed=9, fresh_step2_paths=fresh))
+        assert_report_close(rep, orc)
 
 
 def test_estimate_means_and_std_errors(ref, small):
