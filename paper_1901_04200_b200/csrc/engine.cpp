@@ -154,6 +154,7 @@ struct ltg_ctx {
     RngConsts h_rc{};
     RngTables h_tab{};
     uint32_t seg_steps = 16;  // checkpoint interval of the current call
+    int fp32 = 0;             // precision of the current call (Heston only)
 
     // per-call buffers
     DevBuf d_x, d_targets, d_part1, d_part2, d_groups, d_tot1, d_tot2, d_res, d_grad, d_counter,
@@ -342,6 +343,7 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
     a.tables = c->d_tab.as<RngTables>();
     a.rc = c->h_rc;
     a.seg_steps = c->seg_steps;
+    a.fp32 = c->fp32;
     return a;
 }
 
@@ -372,7 +374,9 @@ void validate_cfg(ltg_ctx* c, const ltg_mc_config* cfg, size_t M) {
                            std::to_string(c->M));
     require(cfg->paths > 0, "forward_pass: paths must be > 0");
     require(cfg->precision == LTG_FP64 || cfg->precision == LTG_FP32, "unknown precision");
-    require(cfg->precision == LTG_FP64, "fp32 precision is not available for this model yet");
+    require(cfg->precision == LTG_FP64 || c->kind == 0,
+            "fp32 precision is implemented for Heston-SLV programs (config 5)");
+    c->fp32 = cfg->precision == LTG_FP32 ? 1 : 0;
 }
 
 void check_params(ltg_ctx* c, const double* x) {
@@ -433,7 +437,7 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                                  : 0;
         for (uint32_t ks : {8u, 16u}) {
             const uint32_t nseg = (c->steps + ks - 1) / ks;
-            const size_t need = size_t(nseg > 1 ? nseg - 1 : 0) * w.ckpt_stride * 16;
+            const size_t need = size_t(nseg > 1 ? nseg - 1 : 0) * w.ckpt_stride * (c->fp32 ? 8 : 16);
             if (need <= avail) {
                 c->seg_steps = ks;
                 if (need > c->d_ckpt.bytes) {
@@ -507,7 +511,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
             if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
             size_t free_b = 0, total_b = 0;
             cudaMemGetInfo(&free_b, &total_b);
-            const size_t per_chunk = size_t(nseg - 1) * plan.chunk_paths * 16;
+            const size_t per_chunk = size_t(nseg - 1) * plan.chunk_paths * (c->fp32 ? 8 : 16);
             size_t budget = c->d_ckpt.bytes;
             if (budget < per_chunk * 64 && free_b > (size_t(2) << 30))
                 budget = std::max(budget, std::min(free_b - (size_t(2) << 30),

@@ -245,6 +245,11 @@ void fill_as241(RngConsts& K) {
          5.99832206555887937690e-1, 1.0}};
     std::memcpy(K.num, num, sizeof num);
     std::memcpy(K.den, den, sizeof den);
+    for (int s = 0; s < 3; ++s)
+        for (int k = 0; k < 8; ++k) {
+            K.fnum[s][k] = (float)num[s][k];
+            K.fden[s][k] = (float)den[s][k];
+        }
 }
 
 }  // namespace ltg

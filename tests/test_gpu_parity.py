@@ -171,6 +171,32 @@ def test_basket_multi_maturity_puts(ref):
         assert_report_close(rep, orc)
 
 
+FP32_TOL = {"means": 1e-4, "G": 1e-3, "grad": 1e-3}   # vs the fp64 oracle, same paths
+
+
+@pytest.mark.parametrize("name,paths", [("cfg3", 1 << 14), ("heston_small", 4096)])
+def test_fp32_mode_against_fp64_oracle(ref, golden_dir, name, paths):
+    # config 5's fp32 variant: float state/adjoint, float AS241 on the same
+    # Philox words; stated tolerance: means 1e-4, G 1e-3,
+    # grad 1e-3 relative with a floor of 1e-3 * max|grad|
+    from paper_1901_04200_b200.model import FP32
+    if name == "heston_small":
+        spec = load_model_spec(f"{golden_dir}/heston_small.json")
+        prog = ref.program(spec)
+        x = prog.initial_params()
+        t = 0.9 * prog.estimate_means(x, paths, 3, workers=8)[0]
+        seed = 3
+    else:
+        c = configs.ALL[name]()
+        spec, x, t, seed = c.spec, c.x, configs.load_targets(c), c.seed
+        prog = ref.program(spec)
+    orc = prog.gradient_of_G(x, t, paths, seed, workers=8)
+    rep = Engine(spec).gradient_of_G(x, t, MCConfig(paths=paths, seed=seed, precision=FP32))
+    assert rel_err(rep.means, orc["means"], 1e-6) <= FP32_TOL["means"]
+    assert rel_err([rep.G], [orc["G"]]) <= FP32_TOL["G"]
+    assert rel_err(rep.grad, orc["grad"], 1e-3) <= FP32_TOL["grad"]
+
+
 def test_estimate_means_and_std_errors(ref, small):
     spec, eng = small
     prog = ref.program(spec)
