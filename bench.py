@@ -233,16 +233,26 @@ def main():
         value = cfg.paths * K / (dev_total * 1e-3)
         e2e = cfg.paths * K / wall
         peak = probe_fp64_rate(local)
-        w2 = census.pass2_fp64_per_path(cfg.name, args.precision)
-        paths_rank = tm["paths_pass2"]
-        achieved = (w2 * paths_rank / (p2_tot / K * 1e-3)) if w2 else None
-        roof = {"bound": "fp64", "kernel": "heston_pass2_kernel",
+        # dominant kernel of the step (device time), its frozen FP64 census
+        dom = "pass2" if p2_tot >= p1_tot else "pass1"
+        basket = not hasattr(cfg.spec, "mc")
+        kname = ("basket_" if basket else "heston_") + dom + "_kernel"
+        w = (census.pass2_fp64_per_path if dom == "pass2" else census.pass1_fp64_per_path)(
+            cfg.name, args.precision)
+        paths_rank = tm["paths_pass2"] if dom == "pass2" else tm["paths_pass1"]
+        t_dom = (p2_tot if dom == "pass2" else p1_tot) / K * 1e-3
+        achieved = (w * paths_rank / t_dom) if w else None
+        w_all = [census.pass1_fp64_per_path(cfg.name, args.precision),
+                 census.pass2_fp64_per_path(cfg.name, args.precision)]
+        roof = {"bound": "fp64", "kernel": kname,
                 "achieved": achieved / 1e12 if achieved else None,
                 "peak": peak / 1e12, "unit": "T fp64-inst/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
-                "census_fp64_per_path": w2,
+                "census_fp64_per_path": w,
+                "whole_step_frac": (sum(w_all) * cfg.paths * K / (dev_total * 1e-3) / peak)
+                if all(w_all) else None,
                 "peak_source": "measured in this run: ltg_probe_fp64_rate (DFMA, 8 chains/thread)"}
-        trf = census.pass2_dram_bytes_per_path(cfg.name, args.precision)
+        trf = census.dram_bytes_per_path(cfg.name, args.precision, dom)
         if trf is not None:
             roof["traffic"] = trf * paths_rank
         M, m = len(cfg.x), cfg.m
@@ -254,8 +264,9 @@ def main():
             "data": "synthetic (seeded Philox paths; no dataset)",
             "config": {"workload": cfg.name, "model": cfg.description, "paths": cfg.paths,
                        "seed": cfg.seed, "parallelism": f"path-sharded dp{world}",
-                       "l2": "working set > L2: HBM checkpoint table "
-                             f"{census.ckpt_bytes(cfg)/1e9:.1f} GB rewritten every step"},
+                       "l2": "working set > L2: HBM checkpoint/store table "
+                             f"{tm['ckpt_bytes']/1e9:.1f} GB rewritten every step",
+                       "checkpoint_interval_steps": tm["seg_steps"]},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * (M + m),
                     "d2h_bytes_per_step": 8 * (1 + 3 * m + M)},
             "gpu_launches": launches,

@@ -144,6 +144,8 @@ typedef struct ltg_timing {
     uint64_t paths_pass1;
     uint64_t paths_pass2;
     uint32_t launches;           /* kernels this library launched in the call */
+    uint32_t seg_steps;          /* checkpoint interval used (Heston), 0 if none */
+    uint64_t ckpt_bytes;         /* HBM checkpoint / store table written by pass 1 */
 } ltg_timing;
 
 /* Path sharding plan: the path set is cut into fixed chunks whose size

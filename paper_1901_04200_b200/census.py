@@ -7,18 +7,25 @@ launch and divided by the launch's path count. Lanes idled by divergence
 are NOT counted, so achieved/peak is the useful fraction of the FP64 pipe.
 Numbers are frozen per (config, precision, kernel) in DESIGN.md §5 and only
 change when the algorithm changes (not when it is tuned).
+
+cfg3/cfg5 are frozen from the first implementation (profiles/r1_v1_cfg3_full.txt),
+which evaluated exactly one AS241 branch per draw. cfg1/cfg2/cfg4 were first
+counted on the v4 kernels (profiles/r1_v4_census.txt), which evaluate the
+central branch on every draw (about 6 FP64 instructions of redundant work per
+tail draw, ~2% of the total) — those fractions are slightly flattering.
 """
 from __future__ import annotations
 
 from .kernels_meta import SEG_STEPS
 
-# per-path thread-level FP64 instruction counts (ncu, profiles/)
-# frozen from the first (v1) implementation, which evaluates exactly one
-# polynomial per draw and log/sqrt only on tail lanes (profiles/r1_v1_cfg3_full.txt)
-PASS2_FP64 = {"cfg3_heston:fp64": 143004.0}
-PASS1_FP64 = {"cfg3_heston:fp64": 107979.0}
-# per-path DRAM bytes of pass 2 (ncu dram__bytes_read+write / paths), latest capture
-PASS2_DRAM = {"cfg3_heston:fp64": 780.8}
+# per-path thread-level FP64 instruction counts
+PASS1_FP64 = {"cfg3_heston:fp64": 107979.0, "cfg1_gbm:fp64": 2394.0,
+              "cfg2_localvol:fp64": 9945.0, "cfg4_basket16:fp64": 67307.0}
+PASS2_FP64 = {"cfg3_heston:fp64": 143004.0, "cfg1_gbm:fp64": 2960.0,
+              "cfg2_localvol:fp64": 12346.0, "cfg4_basket16:fp64": 503.0}
+# per-path DRAM bytes (ncu dram__bytes_read+write / paths), latest capture
+PASS1_DRAM = {"cfg3_heston:fp64": 1457.1}
+PASS2_DRAM = {"cfg3_heston:fp64": 1511.9}
 
 
 def _key(name: str, precision: str):
@@ -26,20 +33,22 @@ def _key(name: str, precision: str):
     return f"{base}:{precision}"
 
 
-def pass2_fp64_per_path(name: str, precision: str = "fp64"):
-    return PASS2_FP64.get(_key(name, precision))
-
-
 def pass1_fp64_per_path(name: str, precision: str = "fp64"):
     return PASS1_FP64.get(_key(name, precision))
 
 
-def pass2_dram_bytes_per_path(name: str, precision: str = "fp64"):
-    return PASS2_DRAM.get(_key(name, precision))
+def pass2_fp64_per_path(name: str, precision: str = "fp64"):
+    return PASS2_FP64.get(_key(name, precision))
+
+
+def dram_bytes_per_path(name: str, precision: str = "fp64", kernel: str = "pass2"):
+    table = PASS1_DRAM if kernel == "pass1" else PASS2_DRAM
+    return table.get(_key(name, precision))
 
 
 def ckpt_bytes(cfg) -> float:
-    """HBM checkpoint table written by pass 1 and read by pass 2."""
+    """HBM checkpoint table of a 16-step interval (upper bound; the engine
+    reports the table it actually wrote in ltg_timing.ckpt_bytes)."""
     spec = cfg.spec
     if not hasattr(spec, "mc"):
         return 0.0

@@ -478,6 +478,13 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     cuda_check(cudaEventRecord(c->ev[2], c->stream), "event");
     c->timing.launches += 3;
     c->timing.paths_pass1 = plan.path_end - plan.path_begin;
+    if (ckpt && c->kind == 0) {
+        const uint64_t nseg = (c->steps + c->seg_steps - 1) / c->seg_steps;
+        c->timing.seg_steps = c->seg_steps;
+        c->timing.ckpt_bytes = (nseg - 1) * w.ckpt_stride * (c->fp32 ? 8 : 16);
+    } else if (ckpt) {
+        c->timing.ckpt_bytes = uint64_t(c->events.size()) * c->n_assets * w.ckpt_stride * 16;
+    }
     return ckpt;
 }
 
