@@ -146,6 +146,7 @@ typedef struct ltg_timing {
     uint32_t launches;           /* kernels this library launched in the call */
     uint32_t seg_steps;          /* checkpoint interval used (Heston), 0 if none */
     uint64_t ckpt_bytes;         /* HBM checkpoint / store table written by pass 1 */
+    uint64_t z_bytes;            /* HBM draw store written by pass 1 (read by pass 2) */
 } ltg_timing;
 
 /* Path sharding plan: the path set is cut into fixed chunks whose size

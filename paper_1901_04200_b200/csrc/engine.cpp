@@ -62,6 +62,11 @@ struct DevBuf {
         cuda_check(cudaMalloc(&p, b), "cudaMalloc");
         bytes = b;
     }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
     template <typename T>
     T* as() const {
         return static_cast<T*>(p);
@@ -158,7 +163,8 @@ struct ltg_ctx {
 
     // per-call buffers
     DevBuf d_x, d_targets, d_part1, d_part2, d_groups, d_tot1, d_tot2, d_res, d_grad, d_counter,
-        d_ckpt, d_normals;
+        d_ckpt, d_ztab, d_normals;
+    uint64_t z_chunks = 0;  // leading local chunks whose draws pass 1 stored
     double* h_stage = nullptr;  // pinned
     size_t h_stage_bytes = 0;
 
@@ -424,32 +430,74 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         cuda_check(cudaEventRecord(c->ev[1], c->stream), "event");
         c->timing.launches += w.n_chunks ? 1 : 0;
     }
-    // checkpoint interval: 8 steps (more resident CTAs in pass 2) when the
-    // table fits in HBM next to a 2 GiB reserve, else 16, else no table
-    // (pass 2 then replays its checkpoints in waves)
+    // HBM plan for pass 2's inputs: the state every KS steps,
+    // plus the draws of as many chunks as fit (pass 2 then reads them instead
+    // of regenerating them). Preference order: every chunk's draws with
+    // KS = 8; every chunk's draws with KS = 16; KS = 8 without draws; KS = 16
+    // with the draws of as many chunks as fit; no table (pass 2 replays its
+    // checkpoints in waves). LTG_CKPT_STEPS / LTG_ZSTORE=0 override (tuning).
     bool ckpt = false;
     c->seg_steps = 16;
+    c->z_chunks = 0;
     if (want_ckpt && c->kind == 0) {
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
-        const size_t avail = free_b + c->d_ckpt.bytes > (size_t(2) << 30)
-                                 ? free_b + c->d_ckpt.bytes - (size_t(2) << 30)
-                                 : 0;
-        for (uint32_t ks : {8u, 16u}) {
+        const size_t reserve = size_t(2) << 30;
+        const size_t held = c->d_ckpt.bytes + c->d_ztab.bytes;
+        const size_t avail = free_b + held > reserve ? free_b + held - reserve : 0;
+        const size_t elem = c->fp32 ? 8 : 16;
+        const uint64_t nloc = w.n_chunks;
+        const size_t z_chunk = size_t(c->steps) * plan.chunk_paths * elem;
+        auto ck_bytes = [&](uint32_t ks) {
             const uint32_t nseg = (c->steps + ks - 1) / ks;
-            const size_t need = size_t(nseg > 1 ? nseg - 1 : 0) * w.ckpt_stride * (c->fp32 ? 8 : 16);
-            if (need <= avail) {
-                c->seg_steps = ks;
-                if (need > c->d_ckpt.bytes) {
-                    c->d_ckpt.ensure(0);
-                    if (c->d_ckpt.p) cudaFree(c->d_ckpt.p);
-                    c->d_ckpt.p = nullptr;
-                    c->d_ckpt.bytes = 0;
-                    c->d_ckpt.ensure(need);
-                }
-                ckpt = nseg > 1;
+            return size_t(nseg > 1 ? nseg - 1 : 0) * w.ckpt_stride * elem;
+        };
+        const char* env_ks = std::getenv("LTG_CKPT_STEPS");
+        const char* env_z = std::getenv("LTG_ZSTORE");
+        const bool z_ok = !(env_z && env_z[0] == '0');
+        const uint32_t forced = env_ks ? (uint32_t)std::atoi(env_ks) : 0u;
+        struct Opt {
+            uint32_t ks;
+            uint64_t z;
+        };
+        std::vector<Opt> opts;
+        if (z_ok) {
+            opts.push_back({8, nloc});
+            opts.push_back({16, nloc});
+        }
+        opts.push_back({8, 0});
+        opts.push_back({16, 0});
+        bool chosen = false;
+        for (const Opt& o : opts) {
+            if (forced && o.ks != forced) continue;
+            if (ck_bytes(o.ks) + o.z * z_chunk <= avail) {
+                c->seg_steps = o.ks;
+                c->z_chunks = o.z;
+                chosen = true;
                 break;
             }
+        }
+        if (!chosen) {
+            const uint32_t ks = forced ? forced : 16u;
+            if (ck_bytes(ks) <= avail) {
+                c->seg_steps = ks;
+                c->z_chunks = z_ok ? std::min<uint64_t>(nloc, (avail - ck_bytes(ks)) / z_chunk) : 0;
+                chosen = true;
+            }
+        }
+        if (const char* cap = std::getenv("LTG_ZCHUNKS_MAX"))  // tests: partial draw store
+            c->z_chunks = std::min<uint64_t>(c->z_chunks, std::strtoull(cap, nullptr, 10));
+        if (chosen) {
+            const size_t need_ck = ck_bytes(c->seg_steps);
+            const size_t need_z = size_t(c->z_chunks) * z_chunk;
+            if (need_ck > c->d_ckpt.bytes || need_z > c->d_ztab.bytes) {
+                c->d_ckpt.release();
+                c->d_ztab.release();
+                c->d_ckpt.ensure(need_ck);
+                c->d_ztab.ensure(need_z);
+            }
+            ckpt = ((c->steps + c->seg_steps - 1) / c->seg_steps) > 1;
+            if (!ckpt) c->z_chunks = 0;
         }
     }
     if (c->kind == 0) {
@@ -459,6 +507,10 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         a.ckpt = ckpt ? c->d_ckpt.as<double2>() : nullptr;
         a.write_sums = 1;
         a.write_ckpt = ckpt ? 1 : 0;
+        a.ztab = c->d_ztab.p;
+        a.z_chunks = c->z_chunks;
+        a.z_stride = std::max<uint64_t>(1, c->z_chunks * plan.chunk_paths);
+        a.write_z = c->z_chunks > 0 ? 1 : 0;
         zero_counter(c, 0);
         cuda_check(cudaEventRecord(c->ev[0], c->stream), "event");
         if (w.n_chunks) cuda_check(launch_heston_pass1(a, w, 0, c->stream), "heston pass 1");
@@ -482,6 +534,7 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         const uint64_t nseg = (c->steps + c->seg_steps - 1) / c->seg_steps;
         c->timing.seg_steps = c->seg_steps;
         c->timing.ckpt_bytes = (nseg - 1) * w.ckpt_stride * (c->fp32 ? 8 : 16);
+        c->timing.z_bytes = c->z_chunks * plan.chunk_paths * c->steps * (c->fp32 ? 8 : 16);
     } else if (ckpt) {
         c->timing.ckpt_bytes = uint64_t(c->events.size()) * c->n_assets * w.ckpt_stride * 16;
     }
@@ -551,6 +604,10 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         } else {
             if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
             a.ckpt = c->d_ckpt.as<double2>();
+            a.ztab = c->d_ztab.p;
+            a.z_chunks = c->z_chunks;
+            a.z_stride = std::max<uint64_t>(1, c->z_chunks * plan.chunk_paths);
+            a.use_z = (c->z_chunks > 0 && !cfg.fresh_step2_paths) ? 1 : 0;
             a.partials = c->d_part2.as<double>() + plan.chunk_begin * c->M;
             zero_counter(c, 2);
             w.counter = c->d_counter.as<uint32_t>() + 2;

@@ -233,6 +233,33 @@ def test_fresh_step2_paths(ref, small):
     assert_report_close(rep, orc)
 
 
+@pytest.mark.parametrize("env", [{"LTG_ZSTORE": "0"}, {"LTG_ZCHUNKS_MAX": "3"},
+                                 {"LTG_CKPT_STEPS": "16"},
+                                 {"LTG_CKPT_STEPS": "16", "LTG_ZSTORE": "0"}])
+def test_memory_plans_bitwise_identical(env):
+    # pass 2 reading stored draws, regenerating them, or mixing both per
+    # chunk, with 8- or 16-step checkpoints: the same arithmetic on the same
+    # draws, so the report must not change by a single bit
+    import os
+    c = configs.cfg3()
+    eng = Engine(c.spec)
+    cfg = MCConfig(paths=5000, seed=c.seed)
+    t = configs.load_targets(c)
+    base = eng.gradient_of_G(c.x, t, cfg)
+    assert eng.timing()["z_bytes"] > 0 and eng.timing()["seg_steps"] == 8
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        rep = eng.gradient_of_G(c.x, t, cfg)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k)
+            else:
+                os.environ[k] = v
+    assert rep.to_json() == base.to_json()
+
+
 def test_lambda_zero_identity(small):
     # test_calibrate.cpp:201-221: targets = means at the truth, same seed
     spec, eng = small

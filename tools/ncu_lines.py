@@ -32,8 +32,10 @@ base = rows[0][0]
 
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
-m = re.search(r"heston_(pass\d)_kernel<(?:\(int\))?(\d+), (?:\(bool\))?(\d)>", kname)
-want = f"heston_{m.group(1)}_kernelILi{m.group(2)}ELb{m.group(3)}E" if m else kern
+m = re.search(r"heston_(pass\d)_kernel<(double|float), (?:\(int\))?(\d+), (?:\(bool\))?(\d)>",
+              kname)
+want = (f"heston_{m.group(1)}_kernelI{m.group(2)[0]}Li{m.group(3)}ELb{m.group(4)}E" if m
+        else kern)
 lines = {}
 for cub in glob.glob(os.path.join(tmp, "*.cubin")):
     dis = subprocess.run(["nvdisasm", "-g", cub], capture_output=True, text=True).stdout
