@@ -1,11 +1,11 @@
 #!/bin/bash
-mkdir -p gpurun_out
-[ -x tools/latency_probe ] && tools/latency_probe
 for v in paper_1901_04200_b200/_lib/variants/*.so; do
-  echo "== $v"; LTG_LIB=$v timeout 120 python tools/quick_time.py cfg3 cfg2 2>&1 | tail -2 | python -c "
+  for env in "LTG_ZSTORE=1" "LTG_ZSTORE=0"; do
+  echo "== $v $env"; env $env LTG_LIB=$v timeout 120 python tools/quick_time.py cfg3 2>&1 | tail -1 | python -c "
 import sys, json
 for l in sys.stdin:
     try:
         d = json.loads(l); print(d['cfg'], 'p1 %.2f p2 %.2f tot %.2f' % (d['pass1_ms'], d['pass2_ms'], d['total_ms']))
     except Exception: print(l.strip()[:200])"
+  done
 done
