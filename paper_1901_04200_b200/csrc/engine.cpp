@@ -80,6 +80,8 @@ struct Nccl {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
@@ -94,10 +96,12 @@ struct Nccl {
         GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
         CommInitRank = reinterpret_cast<decltype(CommInitRank)>(dlsym(lib, "ncclCommInitRank"));
         AllGather = reinterpret_cast<decltype(AllGather)>(dlsym(lib, "ncclAllGather"));
+        AllReduce = reinterpret_cast<decltype(AllReduce)>(dlsym(lib, "ncclAllReduce"));
         CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(lib, "ncclCommDestroy"));
         GetErrorString =
             reinterpret_cast<decltype(GetErrorString)>(dlsym(lib, "ncclGetErrorString"));
-        if (!GetUniqueId || !CommInitRank || !AllGather || !CommDestroy || !GetErrorString) {
+        if (!GetUniqueId || !CommInitRank || !AllGather || !AllReduce || !CommDestroy ||
+            !GetErrorString) {
             why = "libnccl.so.2 lacks required symbols";
             return false;
         }
@@ -124,6 +128,10 @@ ltg_shard make_plan(uint64_t paths, int rank, int world) {
     s.path_end = std::min<uint64_t>(s.chunk_end * s.chunk_paths, paths);
     return s;
 }
+
+// d_counter slots: 0-2 chunk schedulers of the launches, kRareSlot the
+// fast-arithmetic out-of-range flag
+constexpr int kRareSlot = 8;
 
 uint64_t chunks_per_rank(const ltg_shard& s, int world) {
     return (s.n_chunks + world - 1) / world;
@@ -160,6 +168,7 @@ struct ltg_ctx {
     RngTables h_tab{};
     uint32_t seg_steps = 16;  // checkpoint interval of the current call
     int fp32 = 0;             // precision of the current call (Heston only)
+    int safe = 0;             // 1: exact slow paths for every argument (heston_step SAFE)
 
     // per-call buffers
     DevBuf d_x, d_targets, d_part1, d_part2, d_groups, d_tot1, d_tot2, d_res, d_grad, d_counter,
@@ -350,6 +359,8 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
     a.rc = c->h_rc;
     a.seg_steps = c->seg_steps;
     a.fp32 = c->fp32;
+    a.safe = c->safe;
+    a.rare = c->d_counter.as<uint32_t>() + kRareSlot;
     return a;
 }
 
@@ -634,6 +645,35 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
+// The fast arithmetic's out-of-range flag (heston.cu heston_step): cleared
+// before a call, OR-ed across ranks, copied back with the results. A set flag
+// makes the caller redo the call in safe mode.
+int force_safe() {  // LTG_SAFE=1: start in safe mode (tests)
+    const char* e = std::getenv("LTG_SAFE");
+    return e && e[0] == '1' ? 1 : 0;
+}
+
+void clear_rare(ltg_ctx* c) {
+    cuda_check(cudaMemsetAsync(c->d_counter.as<uint32_t>() + kRareSlot, 0, sizeof(uint32_t),
+                               c->stream),
+               "memset");
+}
+
+bool take_rare(ltg_ctx* c, double* host_slot) {
+    uint32_t* d = c->d_counter.as<uint32_t>() + kRareSlot;
+    if (c->world > 1) {
+        const ncclResult_t r = nccl().AllReduce(d, d, 1, ncclUint32, ncclMax, c->comm, c->stream);
+        if (r != ncclSuccess)
+            throw Failure(LTG_ECUDA, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
+    }
+    cuda_check(cudaMemcpyAsync(host_slot, d, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream),
+               "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "synchronize");
+    uint32_t v = 0;
+    std::memcpy(&v, host_slot, sizeof v);
+    return v != 0;
+}
+
 void upload_x(ltg_ctx* c, const double* x, const double* targets) {
     c->h_x.assign(x, x + c->M);
     const size_t n = c->M + (targets ? c->m : 0);
@@ -834,20 +874,25 @@ int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* tar
                 "gradient_of_G: fresh_step2_paths replays nothing, so stored forward state "
                 "cannot be used; switch to recompute mode");
         check_params(ctx, x);
-        ctx->timing = ltg_timing{};
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
-        upload_x(ctx, x, targets);
-        const bool ckpt = run_pass1(ctx, *cfg, plan, true, !cfg->fresh_step2_paths);
-        run_pass2(ctx, *cfg, plan, ckpt);
         const uint32_t nm = ctx->m;
-        double* st = ctx->stage(1 + 3 * nm + ctx->M);
-        cuda_check(cudaMemcpyAsync(st, ctx->d_res.p, (1 + 3 * nm) * 8, cudaMemcpyDeviceToHost,
-                                   ctx->stream),
-                   "D2H");
-        cuda_check(cudaMemcpyAsync(st + 1 + 3 * nm, ctx->d_grad.p, ctx->M * 8,
-                                   cudaMemcpyDeviceToHost, ctx->stream),
-                   "D2H");
-        cuda_check(cudaStreamSynchronize(ctx->stream), "gradient_of_G");
+        double* st = nullptr;
+        for (ctx->safe = force_safe();; ctx->safe = 1) {
+            ctx->timing = ltg_timing{};
+            upload_x(ctx, x, targets);
+            clear_rare(ctx);
+            const bool ckpt = run_pass1(ctx, *cfg, plan, true, !cfg->fresh_step2_paths);
+            run_pass2(ctx, *cfg, plan, ckpt);
+            st = ctx->stage(2 + 3 * nm + ctx->M);
+            cuda_check(cudaMemcpyAsync(st, ctx->d_res.p, (1 + 3 * nm) * 8,
+                                       cudaMemcpyDeviceToHost, ctx->stream),
+                       "D2H");
+            cuda_check(cudaMemcpyAsync(st + 1 + 3 * nm, ctx->d_grad.p, ctx->M * 8,
+                                       cudaMemcpyDeviceToHost, ctx->stream),
+                       "D2H");
+            if (!take_rare(ctx, st + 1 + 3 * nm + ctx->M) || ctx->safe) break;
+        }
+        ctx->safe = 0;
         ctx->timing.pass1_ms = elapsed(ctx->ev[0], ctx->ev[1]);
         ctx->timing.pass2_ms = elapsed(ctx->ev[3], ctx->ev[4]);
         ctx->timing.reduce_ms = elapsed(ctx->ev[1], ctx->ev[2]) + elapsed(ctx->ev[4], ctx->ev[5]);
@@ -873,16 +918,21 @@ int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_con
         validate_cfg(ctx, cfg, M);
         require(x && means, "null buffer");
         check_params(ctx, x);
-        ctx->timing = ltg_timing{};
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
-        upload_x(ctx, x, nullptr);
-        run_pass1(ctx, *cfg, plan, false, false);
         const uint32_t nm = ctx->m;
-        double* st = ctx->stage(1 + 3 * nm);
-        cuda_check(cudaMemcpyAsync(st, ctx->d_res.p, (1 + 3 * nm) * 8, cudaMemcpyDeviceToHost,
-                                   ctx->stream),
-                   "D2H");
-        cuda_check(cudaStreamSynchronize(ctx->stream), "estimate_means");
+        double* st = nullptr;
+        for (ctx->safe = force_safe();; ctx->safe = 1) {
+            ctx->timing = ltg_timing{};
+            upload_x(ctx, x, nullptr);
+            clear_rare(ctx);
+            run_pass1(ctx, *cfg, plan, false, false);
+            st = ctx->stage(2 + 3 * nm);
+            cuda_check(cudaMemcpyAsync(st, ctx->d_res.p, (1 + 3 * nm) * 8,
+                                       cudaMemcpyDeviceToHost, ctx->stream),
+                       "D2H");
+            if (!take_rare(ctx, st + 1 + 3 * nm) || ctx->safe) break;
+        }
+        ctx->safe = 0;
         ctx->timing.pass1_ms = elapsed(ctx->ev[0], ctx->ev[1]);
         ctx->timing.reduce_ms = elapsed(ctx->ev[1], ctx->ev[2]);
         ctx->timing.total_ms = elapsed(ctx->ev[0], ctx->ev[2]);
@@ -975,11 +1025,13 @@ int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int
         ctx->d_normals.ensure(npaths * ctx->m * 8);
         zero_counter(ctx, 0);
         if (ctx->kind == 0) {
+            ctx->fp32 = 0;
             HestonArgs a = heston_args(ctx, ctx->h_x.data());
             a.partials = ctx->d_part1.as<double>();
             a.path_out = ctx->d_normals.as<double>();
             a.write_sums = 1;
             a.write_ckpt = 0;
+            a.safe = 1;  // diagnostic entry: exact slow paths throughout
             cuda_check(launch_heston_pass1(a, w, 0, ctx->stream), "path payoffs");
         } else {
             BasketArgs b = basket_args(ctx, ctx->h_x.data());

@@ -245,6 +245,10 @@ void fill_as241(RngConsts& K) {
          5.99832206555887937690e-1, 1.0}};
     std::memcpy(K.num, num, sizeof num);
     std::memcpy(K.den, den, sizeof den);
+    K.lit_uniform = -0x1.fffffffffffffp-1;
+    K.lit_qmax = 0.425;
+    K.lit_central = 0.180625;
+    K.lit_tail1 = 1.6;
     for (int s = 0; s < 3; ++s)
         for (int k = 0; k < 8; ++k) {
             K.fnum[s][k] = (float)num[s][k];

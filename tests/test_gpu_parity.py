@@ -235,7 +235,8 @@ def test_fresh_step2_paths(ref, small):
 
 @pytest.mark.parametrize("env", [{"LTG_ZSTORE": "0"}, {"LTG_ZCHUNKS_MAX": "3"},
                                  {"LTG_CKPT_STEPS": "16"},
-                                 {"LTG_CKPT_STEPS": "16", "LTG_ZSTORE": "0"}])
+                                 {"LTG_CKPT_STEPS": "16", "LTG_ZSTORE": "0"},
+                                 {"LTG_SAFE": "1"}])
 def test_memory_plans_bitwise_identical(env):
     # pass 2 reading stored draws, regenerating them, or mixing both per
     # chunk, with 8- or 16-step checkpoints: the same arithmetic on the same

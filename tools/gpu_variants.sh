@@ -1,7 +1,7 @@
 #!/bin/bash
-for v in paper_1901_04200_b200/_lib/variants/*.so; do
+for v in "" paper_1901_04200_b200/_lib/variants/*.so; do
   for env in "LTG_ZSTORE=1" "LTG_ZSTORE=0"; do
-  echo "== $v $env"; env $env LTG_LIB=$v timeout 120 python tools/quick_time.py cfg3 2>&1 | tail -1 | python -c "
+  echo "== $v $env"; env $env ${v:+LTG_LIB=$v} timeout 120 python tools/quick_time.py cfg3 2>&1 | tail -1 | python -c "
 import sys, json
 for l in sys.stdin:
     try:
