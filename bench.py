@@ -251,7 +251,8 @@ def main():
                 "census_fp64_per_path": w,
                 "whole_step_frac": (sum(w_all) * cfg.paths * K / (dev_total * 1e-3) / peak)
                 if all(w_all) else None,
-                "peak_source": "measured in this run: ltg_probe_fp64_rate (DFMA, 8 chains/thread)"}
+                "peak_source": "measured in this run: ltg_probe_fp64_rate (fastest of DFMA, "
+                               "DMUL+DADD, DADD streams; 8 chains/thread, full occupancy)"}
         trf = census.dram_bytes_per_path(cfg.name, args.precision, dom)
         if trf is not None:
             roof["traffic"] = trf * paths_rank

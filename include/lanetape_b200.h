@@ -208,10 +208,11 @@ int ltg_shard_plan(uint64_t paths, int rank, int world, ltg_shard* out);
 int ltg_nccl_unique_id(unsigned char id[128]);
 int ltg_attach_nccl(ltg_ctx* ctx, const unsigned char id[128], int rank, int world);
 
-/* Diagnostic: measured FP64 DFMA issue rate of `device` (thread-DFMAs per
- * second, 8 independent chains per thread, best of 5) — the roofline
- * denominator reported by bench.py. */
-int ltg_probe_fp64_rate(int device, double* dfma_per_s, double* sm_clock_hz);
+/* Diagnostic: measured FP64 issue rate of `device` — thread-level FP64
+ * instructions per second, the fastest of DFMA, DMUL+DADD and DADD streams
+ * (8 independent chains per thread, full occupancy, best of 3) — the
+ * roofline denominator reported by bench.py. */
+int ltg_probe_fp64_rate(int device, double* fp64_per_s, double* sm_clock_hz);
 
 /* Host-only self-test of the random stream's log(): locates and validates
  * the host libm table (as context creation does) and compares the GPU's

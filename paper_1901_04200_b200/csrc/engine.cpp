@@ -279,7 +279,7 @@ size_t floor_index(const std::vector<double>& nodes, double x) {
 }
 
 void all_gather_rows(ltg_ctx* c, double* table, uint64_t per_rank, uint32_t width) {
-    if (c->world <= 1) return;
+    if (!c->comm) return;  // (an attached single-rank comm still runs the collective)
     const size_t count = size_t(per_rank) * width;
     const ncclResult_t r = nccl().AllGather(table + size_t(c->rank) * count, table, count,
                                             ncclFloat64, c->comm, c->stream);
@@ -661,7 +661,7 @@ void clear_rare(ltg_ctx* c) {
 
 bool take_rare(ltg_ctx* c, double* host_slot) {
     uint32_t* d = c->d_counter.as<uint32_t>() + kRareSlot;
-    if (c->world > 1) {
+    if (c->comm) {
         const ncclResult_t r = nccl().AllReduce(d, d, 1, ncclUint32, ncclMax, c->comm, c->stream);
         if (r != ncclSuccess)
             throw Failure(LTG_ECUDA, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));

@@ -75,7 +75,7 @@ def load_library(path: str = LIB_PATH):
 
 
 def probe_fp64_rate(device: int = 0) -> float:
-    """Measured DFMA issue rate (thread-DFMAs/s) of the GPU."""
+    """Measured FP64 issue rate (thread FP64 instructions/s) of the GPU."""
     L = load_library()
     r, clk = C.c_double(), C.c_double()
     if L.ltg_probe_fp64_rate(device, C.byref(r), C.byref(clk)):

@@ -261,6 +261,19 @@ def test_memory_plans_bitwise_identical(env):
     assert rep.to_json() == base.to_json()
 
 
+def test_nccl_attached_single_rank_bitwise():
+    # the multi-GPU code path (run-time NCCL, in-place all-gather of the chunk
+    # tables, all-reduce of the rare flag) on a one-rank communicator
+    from paper_1901_04200_b200.engine import nccl_unique_id
+    c = configs.cfg3()
+    t = configs.load_targets(c)
+    cfg = MCConfig(paths=4099, seed=c.seed)
+    base = Engine(c.spec).gradient_of_G(c.x, t, cfg)
+    eng = Engine(c.spec)
+    eng.attach_nccl(nccl_unique_id(), 0, 1)
+    assert eng.gradient_of_G(c.x, t, cfg).to_json() == base.to_json()
+
+
 def test_lambda_zero_identity(small):
     # test_calibrate.cpp:201-221: targets = means at the truth, same seed
     spec, eng = small
