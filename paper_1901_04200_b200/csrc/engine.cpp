@@ -443,10 +443,9 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     }
     // HBM plan for pass 2's inputs: the state every KS steps,
     // plus the draws of as many chunks as fit (pass 2 then reads them instead
-    // of regenerating them). Preference order: every chunk's draws with
-    // KS = 8; every chunk's draws with KS = 16; KS = 8 without draws; KS = 16
-    // with the draws of as many chunks as fit; no table (pass 2 replays its
-    // checkpoints in waves). LTG_CKPT_STEPS / LTG_ZSTORE=0 override (tuning).
+    // of regenerating them): KS = 8 if its table fits, else KS = 16, else no
+    // table (pass 2 replays its checkpoints in waves). LTG_CKPT_STEPS /
+    // LTG_ZSTORE=0 override (tuning).
     bool ckpt = false;
     c->seg_steps = 16;
     c->z_chunks = 0;
@@ -467,34 +466,17 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         const char* env_z = std::getenv("LTG_ZSTORE");
         const bool z_ok = !(env_z && env_z[0] == '0');
         const uint32_t forced = env_ks ? (uint32_t)std::atoi(env_ks) : 0u;
-        struct Opt {
-            uint32_t ks;
-            uint64_t z;
-        };
-        std::vector<Opt> opts;
-        if (z_ok) {
-            opts.push_back({8, nloc});
-            opts.push_back({16, nloc});
-        }
-        opts.push_back({8, 0});
-        opts.push_back({16, 0});
+        // the first interval whose checkpoint table fits, with the draws of as
+        // many chunks as the rest of HBM holds (KS = 8 halves the replay
+        // buffers of KS = 16 and keeps 5 pass-2 CTAs per SM resident)
         bool chosen = false;
-        for (const Opt& o : opts) {
-            if (forced && o.ks != forced) continue;
-            if (ck_bytes(o.ks) + o.z * z_chunk <= avail) {
-                c->seg_steps = o.ks;
-                c->z_chunks = o.z;
-                chosen = true;
-                break;
-            }
-        }
-        if (!chosen) {
-            const uint32_t ks = forced ? forced : 16u;
-            if (ck_bytes(ks) <= avail) {
-                c->seg_steps = ks;
-                c->z_chunks = z_ok ? std::min<uint64_t>(nloc, (avail - ck_bytes(ks)) / z_chunk) : 0;
-                chosen = true;
-            }
+        for (uint32_t ks : {8u, 16u}) {
+            if (forced && ks != forced) continue;
+            if (ck_bytes(ks) > avail) continue;
+            c->seg_steps = ks;
+            c->z_chunks = z_ok ? std::min<uint64_t>(nloc, (avail - ck_bytes(ks)) / z_chunk) : 0;
+            chosen = true;
+            break;
         }
         if (const char* cap = std::getenv("LTG_ZCHUNKS_MAX"))  // tests: partial draw store
             c->z_chunks = std::min<uint64_t>(c->z_chunks, std::strtoull(cap, nullptr, 10));
