@@ -185,6 +185,13 @@ int ltg_finite_diff_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const
 int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, uint64_t path0,
                      uint64_t npaths, double* out);
 
+/* inverse_normal_cdf (rng.hpp:45-85) of n uniforms p[i] through the device
+ * AS241 (central and both tail rows; the path kernels run the same code fused
+ * with Philox). p must lie in (0,1) (LTG_EINVAL otherwise, where the reference
+ * throws) and be of the generator's form (2k+1)*2^-53, which makes q = p - 0.5
+ * exact as in the reference. Diagnostic / parity entry point. */
+int ltg_inverse_normal(ltg_ctx* ctx, const double* p, size_t n, double* z);
+
 /* Per-path outputs of the program (forward_eval, tape.hpp:276-331, on the
  * draws PhiloxNormalSource(seed).fill(p)) for p in [path0, path0+npaths):
  * y is npaths*m, path-major. */

@@ -246,6 +246,7 @@ void init_common(ltg_ctx* c, int device) {
     for (auto& e : c->ev) cuda_check(cudaEventCreate(&e), "event");
     fill_as241(c->h_rc);
     c->rng_note = discover_glibc_math(c->h_rc, c->h_tab);
+    for (int k = 0; k < 8; ++k) c->h_tab.as241_far[k] = make_double2(c->h_rc.num[2][k], c->h_rc.den[2][k]);
     c->d_tab.ensure(sizeof(RngTables));
     cuda_check(cudaMemcpy(c->d_tab.p, &c->h_tab, sizeof(RngTables), cudaMemcpyHostToDevice),
                "rng upload");
@@ -982,6 +983,24 @@ int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, ui
                                    ctx->stream),
                    "D2H");
         cuda_check(cudaStreamSynchronize(ctx->stream), "fill_normals");
+    });
+}
+
+int ltg_inverse_normal(ltg_ctx* ctx, const double* p, size_t n, double* z) {
+    if (!ctx) return LTG_EINVAL;
+    return guarded(ctx, [&] {
+        require(p && z, "null buffer");
+        if (n == 0) return;
+        for (size_t i = 0; i < n; ++i)  // rng.hpp:46 throws outside (0, 1)
+            require(p[i] > 0.0 && p[i] < 1.0, "inverse_normal_cdf: p outside (0,1)");
+        ctx->d_normals.ensure(2 * n * 8);
+        double* d_p = ctx->d_normals.as<double>();
+        cuda_check(cudaMemcpyAsync(d_p, p, n * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        cuda_check(launch_inverse_normal(ctx->d_tab.as<RngTables>(), ctx->h_rc, d_p, n, d_p + n,
+                                         ctx->stream),
+                   "inverse_normal");
+        cuda_check(cudaMemcpyAsync(z, d_p + n, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "inverse_normal");
     });
 }
 

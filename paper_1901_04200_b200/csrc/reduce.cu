@@ -105,6 +105,20 @@ __global__ void __launch_bounds__(kBlock) fill_normals_kernel(
     }
 }
 
+// inverse_normal_cdf (rng.hpp:45-85) of given uniforms through the device
+// AS241 (diagnostic: the path kernels fuse it with Philox in gen_segment).
+// p must be of the generator's form (2n+1)*2^-53, so q = p - 0.5 is exact.
+__global__ void inverse_normal_kernel(const RngTables* tables, RngConsts rc, const double* p,
+                                      uint64_t n, double* z) {
+    __shared__ RngTables sh;
+    load_tables(&sh, tables);
+    __syncthreads();
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double q = __dsub_rn(p[i], 0.5);
+    z[i] = fabs(q) <= rc.lit_qmax ? as241_central(q, rc) : as241_tail(q, sh, rc);
+}
+
 }  // namespace
 
 cudaError_t launch_reduce_chunks(const double* table, uint64_t n_chunks, uint32_t width,
@@ -135,6 +149,13 @@ cudaError_t launch_fill_normals(const RngTables* tables, const RngConsts& rc, ui
     if (npaths == 0 || dim == 0) return cudaSuccess;
     fill_normals_kernel<<<(unsigned)((npaths + kBlock - 1) / kBlock), kBlock, 0, s>>>(
         tables, rc, seed_lo, seed_hi, antithetic, path0, npaths, dim, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inverse_normal(const RngTables* tables, const RngConsts& rc, const double* p,
+                                   uint64_t n, double* z, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    inverse_normal_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(tables, rc, p, n, z);
     return cudaGetLastError();
 }
 

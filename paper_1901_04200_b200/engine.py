@@ -61,6 +61,7 @@ def load_library(path: str = LIB_PATH):
                                                 C.POINTER(MCConfigC), C.c_double, _dp]
     L.ltg_fill_normals.argtypes = [C.c_void_p, C.c_uint64, C.c_size_t, C.c_int, C.c_uint64,
                                    C.c_uint64, _dp]
+    L.ltg_inverse_normal.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp]
     L.ltg_last_timing.argtypes = [C.c_void_p, C.POINTER(TimingC)]
     L.ltg_path_payoffs.argtypes = [C.c_void_p, _dp, C.c_size_t, C.c_uint64, C.c_int, C.c_uint64,
                                    C.c_uint64, _dp]
@@ -214,6 +215,16 @@ class Engine:
         if rc:
             self._raise(rc)
         return out
+
+    def inverse_normal(self, p) -> np.ndarray:
+        """inverse_normal_cdf(p) elementwise on the GPU (rng.hpp:45-85); p of the
+        generator's form (2k+1)*2^-53 in (0, 1)."""
+        pa = _arr(p)
+        z = np.empty(pa.size)
+        rc = self.lib.ltg_inverse_normal(self.h, _p(pa), pa.size, _p(z))
+        if rc:
+            self._raise(rc)
+        return z
 
     def path_payoffs(self, x, seed: int, antithetic: bool, path0: int, npaths: int) -> np.ndarray:
         """Per-path program outputs for the draws of paths [path0, path0+npaths)."""

@@ -79,6 +79,40 @@ def test_normals_bulk_tail_exact(ref, small):
     assert np.array_equal(g.view(np.uint64), r.view(np.uint64))
 
 
+def _gen_uniform(k):
+    """The generator's uniforms: (2k+1)*2^-53, k a 52-bit integer (rng.hpp:38-40)."""
+    return (2.0 * np.asarray(k, dtype=np.float64) + 1.0) * 2.0 ** -53
+
+
+def test_inverse_normal_all_rows_bit_exact(ref, small):
+    # every AS241 row on the device, including the r > 5 row that Philox
+    # practically never reaches (p < 1.4e-11) and the generator's endpoints
+    # 2^-53 / 1 - 2^-53 (test_rng.cpp:38-45)
+    top = (1 << 52) - 1
+    rng = np.random.default_rng(1901)
+    ks = [0, 1, 2, 3, top, top - 1, top - 7, 1 << 51, (1 << 51) - 1]
+    for p in (1e-300, 1e-16, 1e-12, 1.388e-11, 1.389e-11, 1e-10, 1e-6, 0.0749999, 0.0750001,
+              0.3, 0.5):
+        k = int(p * 2.0 ** 52)
+        ks += [k, k + 1, top - k, top - k - 1]
+    ks += list(rng.integers(0, 1 << 52, 20000))  # mixed central / tail
+    ks += list(rng.integers(0, 1 << 28, 2000))   # deep lower tail (r > 5 included)
+    ks += list(top - rng.integers(0, 1 << 28, 2000))
+    p = _gen_uniform(np.clip(np.asarray(ks, dtype=np.int64), 0, top))
+    z = small[1].inverse_normal(p)
+    r = np.array([ref.inverse_normal_cdf(float(v)) for v in p])
+    assert np.sum(np.minimum(p, 1 - p) < 1.38e-11) > 10  # the r > 5 row was exercised
+    mism = np.flatnonzero(z.view(np.uint64) != r.view(np.uint64))
+    assert mism.size == 0, [(p[i], z[i], r[i]) for i in mism[:5]]
+
+
+def test_inverse_normal_domain(small):
+    with pytest.raises(ValueError):
+        small[1].inverse_normal([0.5, 0.0])
+    with pytest.raises(ValueError):
+        small[1].inverse_normal([1.0])
+
+
 @pytest.mark.parametrize("name", ["heston_small", "cfg1", "cfg2", "cfg3", "cfg4"])
 def test_per_path_payoffs_bit_exact(ref, golden_dir, name):
     # the GPU forward replays the reference's tape arithmetic operation for
