@@ -1,5 +1,6 @@
 #!/bin/bash
-# One gpurun session: smoke, tests, bench lines, ncu launch list + full capture.
+# One gpurun session: smoke, tests, bench lines, ncu launch list of the default
+# bench command, ncu --set full captures, FP64 census of the other configs.
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/gpu.txt
 nproc >> gpurun_out/gpu.txt; lscpu | grep "Model name" >> gpurun_out/gpu.txt
@@ -11,11 +12,17 @@ timeout 600 python bench.py --precision fp32 --no-cpu-baseline > gpurun_out/benc
 for c in cfg1 cfg2 cfg3 cfg4; do
   timeout 300 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
-CMD="python bench.py --config cfg3 --steps 2 --warmup 3 --no-cpu-baseline"
-$CMD > gpurun_out/plain_cfg3.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg3.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+# launch list of the default bench command (serialised, cold-cache per launch)
+CMD="python bench.py --steps 2 --warmup 3"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_cfg5.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 M=smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_fp64_pred_on.sum,smsp__sass_thread_inst_executed_op_fp32_pred_on.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
+# full captures at 2^20 paths: without the draw store (the regime of 91% of
+# cfg5's chunks on one GPU) and with it (cfg3 default)
 PCMD="python tools/profile_case.py --config cfg3 --paths 1048576"
+LTG_ZSTORE=0 $PCMD > gpurun_out/plain_profile_noz.log 2>&1 && \
+  LTG_ZSTORE=0 timeout 900 ncu --set full --import-source on --clock-control none -k regex:heston_pass -c 2 \
+    --metrics $M -o gpurun_out/prof_cfg3_noz -f $PCMD > gpurun_out/ncu_full_noz.log 2>&1
 $PCMD > gpurun_out/plain_profile.log 2>&1 && \
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:heston_pass -c 2 \
     --metrics $M -o gpurun_out/prof_cfg3_full -f $PCMD > gpurun_out/ncu_full.log 2>&1
