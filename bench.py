@@ -164,6 +164,11 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=4.0,
                     help="target time of one --impl reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--method", default="adjoint", choices=["adjoint", "tangent"],
+                    help="adjoint: the reference's two-pass scheme (the headline); tangent: "
+                         "pass 2 replaced by pathwise forward tangents (small-M Heston only)")
+    ap.add_argument("--no-alt-method", action="store_true",
+                    help="skip the extra tangent-mode measurement reported under alt_methods")
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
     rank, world, local = dist_env()
@@ -201,7 +206,7 @@ def main():
                   precision=FP32 if args.precision == "fp32" else FP64)
 
     for _ in range(args.warmup):
-        eng.gradient_of_G(cfg.x, targets, mc)
+        eng.gradient_of_G(cfg.x, targets, mc, method=args.method)
 
     # ---- timed region: K full gradient_of_G calls ----
     if pg:
@@ -210,7 +215,8 @@ def main():
     with Clocks(local) as clk:
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            rep = eng.gradient_of_G(cfg.x, targets, mc)   # host buffers in, report out, synced
+            # host buffers in, report out, synced
+            rep = eng.gradient_of_G(cfg.x, targets, mc, method=args.method)
             tm = eng.timing()
             dev_ms.append(tm["total_ms"])
             p1_ms.append(tm["pass1_ms"])
@@ -227,6 +233,39 @@ def main():
     else:
         p2_tot, p1_tot = sum(p2_ms), sum(p1_ms)
 
+    # ---- the same workload through the tangent-mode alternative (reported
+    # beside the headline, never instead of it) ----
+    alt = None
+    if args.method == "adjoint" and not args.no_alt_method:
+        try:
+            rt = eng.gradient_of_G(cfg.x, targets, mc, method="tangent")
+        except ValueError:  # not a small-M fp64 Heston model: adjoint only
+            rt = None
+        if rt is not None:
+            for _ in range(max(0, args.warmup - 1)):
+                eng.gradient_of_G(cfg.x, targets, mc, method="tangent")
+            if pg:
+                pg.barrier()
+            t_dev, t0 = 0.0, time.perf_counter()
+            for _ in range(args.steps):
+                rt = eng.gradient_of_G(cfg.x, targets, mc, method="tangent")
+                t_dev += eng.timing()["total_ms"]
+            t_wall = time.perf_counter() - t0
+            if pg:
+                import torch
+                t = torch.tensor([t_dev, t_wall], dtype=torch.float64)
+                pg.all_reduce(t, op=pg.ReduceOp.MAX)
+                t_dev, t_wall = t.tolist()
+            diff = max(abs(a - b) / max(abs(a), abs(b), 1e-12 * max(map(abs, rep.grad)))
+                       for a, b in zip(rt.grad, rep.grad))
+            alt = {"tangent": {
+                "value": cfg.paths * args.steps / (t_dev * 1e-3), "unit": UNIT,
+                "e2e": cfg.paths * args.steps / t_wall, "ms_per_step": t_dev / args.steps,
+                "grad_rel_diff_vs_adjoint": diff,
+                "what": "pass 2 replaced by pathwise forward tangents "
+                        "(ltg_gradient_of_G_tangent): same paths and estimator, "
+                        "grad = sum_i lambda_i J_i / P"}}
+
     out = None
     if rank == 0:
         K = args.steps
@@ -239,11 +278,15 @@ def main():
         kname = ("basket_" if basket else "heston_") + dom + "_kernel"
         w = (census.pass2_fp64_per_path if dom == "pass2" else census.pass1_fp64_per_path)(
             cfg.name, args.precision)
+        if args.method == "tangent":  # one forward+tangent kernel; no frozen census
+            kname, w = "heston_tangent_kernel", None
         paths_rank = tm["paths_pass2"] if dom == "pass2" else tm["paths_pass1"]
         t_dom = (p2_tot if dom == "pass2" else p1_tot) / K * 1e-3
         achieved = (w * paths_rank / t_dom) if w else None
         w_all = [census.pass1_fp64_per_path(cfg.name, args.precision),
                  census.pass2_fp64_per_path(cfg.name, args.precision)]
+        if args.method == "tangent":
+            w_all = [None]
         roof = {"bound": "fp64", "kernel": kname,
                 "achieved": achieved / 1e12 if achieved else None,
                 "peak": peak / 1e12, "unit": "T fp64-inst/s",
@@ -274,6 +317,7 @@ def main():
             "clocks": clocks,
             "roofline": roof,
             "pass_ms": {"pass1": p1_tot / K, "pass2": p2_tot / K},
+            "method": args.method,
             "G": rep.G,
             "rng_exact": eng.rng_exact,
         }
@@ -289,6 +333,8 @@ def main():
             except Exception as e:  # the oracle is optional on the box
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": workers,
                                         "kind": "reference", "sample": f"unavailable: {e}"}
+        if alt:
+            line["alt_methods"] = alt
         out = line
         print(json.dumps(out), flush=True)
     if pg:

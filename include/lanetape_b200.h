@@ -175,6 +175,17 @@ int ltg_pack_params(const ltg_ctx* ctx, double* x, size_t M);
 
 int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets, size_t m,
                       const ltg_mc_config* cfg, ltg_report* report);
+/* The same report as ltg_gradient_of_G, with pass 2 replaced by pathwise
+ * tangents (forward mode): ∇G is linear in λ, so one forward sweep that
+ * carries d(log S)/dx and dV/dx for every parameter gives, per instrument i,
+ * J_i = Σ_p ∂y_i/∂x and then grad = Σ_i λ_i J_i / P — the reference's
+ * estimator on the same paths, same derivative conventions, different
+ * summation order (agrees with ltg_gradient_of_G to ~1e-14). Cheaper than the
+ * adjoint when M is small: fp64 Heston models with one leverage column and at
+ * most 4 leverage rows (M = 5 + rows <= 9); LTG_EINVAL otherwise. Not a
+ * reference interface: an engine alternative to expectation.hpp:300-351. */
+int ltg_gradient_of_G_tangent(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
+                              size_t m, const ltg_mc_config* cfg, ltg_report* report);
 int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg,
                        double* means, double* std_errors);
 int ltg_finite_diff_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets,

@@ -344,6 +344,9 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
         volatile double sq = std::sqrt(c->dt);
         a.sc.rc = su * sq;
         a.sqdt = sq;
+        // tangent mode: d rho_comp / d rho = -rho * sqrt(dt) / sqrt(1 - rho^2)
+        // (0 where the sqrt's argument is 0: the tape's sqrt-at-0 convention)
+        a.drc = su > 0.0 ? -(x[3] * sq) / su : 0.0;
     }
     a.sc.dt = c->dt;
     a.sc.sqdt = a.sqdt;
@@ -622,6 +625,56 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     c->timing.paths_pass2 = plan.path_end - plan.path_begin;
 }
 
+// Tangent mode (ltg_gradient_of_G_tangent): one forward launch over the
+// pass-2 path set carrying the parameter tangents; rows [sum | sumsq | J].
+// With `sums` the same launch also provides pass 1 (means, lambda, G);
+// otherwise (fresh_step2_paths) pass 1 ran before and only J is used.
+void run_tangent(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool sums) {
+    const uint64_t per = chunks_per_rank(plan, c->world);
+    const uint64_t table_rows = per * c->world;
+    const uint32_t width = 2 * c->m + c->m * (uint32_t)c->M;
+    c->d_part2.ensure(table_rows * width * 8);
+    c->d_groups.ensure(((plan.n_chunks + kGroup - 1) / kGroup) * width * 8 + 8);
+    c->d_tot2.ensure(width * 8);
+    c->d_res.ensure((1 + 3 * c->m) * 8);
+    c->d_grad.ensure(c->M * 8);
+    HestonArgs a = heston_args(c, c->h_x.data());
+    a.partials = c->d_part2.as<double>() + plan.chunk_begin * width;
+    a.write_sums = sums ? 1 : 0;
+    Work w = base_work(c, cfg, plan);
+    if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
+    zero_counter(c, 2);
+    w.counter = c->d_counter.as<uint32_t>() + 2;
+    cuda_check(cudaEventRecord(c->ev[sums ? 0 : 3], c->stream), "event");
+    if (w.n_chunks) cuda_check(launch_heston_tangent(a, w, 0, c->stream), "heston tangent");
+    cuda_check(cudaEventRecord(c->ev[sums ? 1 : 4], c->stream), "event");
+    c->timing.launches += w.n_chunks ? 1 : 0;
+    all_gather_rows(c, c->d_part2.as<double>(), per, width);
+    cuda_check(launch_reduce_chunks(c->d_part2.as<double>(), plan.n_chunks, width,
+                                    c->d_groups.as<double>(), c->d_tot2.as<double>(), c->stream),
+               "reduce");
+    c->timing.launches += 2;
+    if (sums) {
+        cuda_check(launch_finalize_means(c->d_tot2.as<double>(), c->m, cfg.paths,
+                                         c->d_targets.as<double>(), c->d_res.as<double>(),
+                                         c->stream),
+                   "finalize");
+        c->timing.launches += 1;
+        c->timing.paths_pass1 = plan.path_end - plan.path_begin;
+        cuda_check(cudaEventRecord(c->ev[2], c->stream), "event");
+        cuda_check(cudaEventRecord(c->ev[3], c->stream), "event");
+        cuda_check(cudaEventRecord(c->ev[4], c->stream), "event");
+    }
+    cuda_check(launch_finalize_grad_tangent(c->d_tot2.as<double>() + 2 * c->m,
+                                            c->d_res.as<double>() + 1 + 2 * c->m, c->m,
+                                            (uint32_t)c->M, cfg.paths, c->d_grad.as<double>(),
+                                            c->stream),
+               "finalize grad");
+    cuda_check(cudaEventRecord(c->ev[5], c->stream), "event");
+    c->timing.launches += 1;
+    c->timing.paths_pass2 = plan.path_end - plan.path_begin;
+}
+
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
@@ -844,8 +897,10 @@ int ltg_shard_plan(uint64_t paths, int rank, int world, ltg_shard* out) {
     return LTG_OK;
 }
 
-int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets, size_t m,
-                      const ltg_mc_config* cfg, ltg_report* report) {
+namespace {
+
+int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets, size_t m,
+                  const ltg_mc_config* cfg, ltg_report* report, bool tangent) {
     if (!ctx) return LTG_EINVAL;
     return guarded(ctx, [&] {
         validate_cfg(ctx, cfg, M);
@@ -856,6 +911,11 @@ int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* tar
         require(!(cfg->memory_mode == LTG_MODE_STORE && cfg->fresh_step2_paths),
                 "gradient_of_G: fresh_step2_paths replays nothing, so stored forward state "
                 "cannot be used; switch to recompute mode");
+        if (tangent)
+            require(ctx->kind == 0 && cfg->precision == LTG_FP64 &&
+                        heston_tangent_supported(ctx->cols, ctx->nlev),
+                    "gradient_of_G_tangent: fp64 Heston models with one leverage column and at "
+                    "most 4 leverage rows (M <= 9); use ltg_gradient_of_G");
         check_params(ctx, x);
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
         const uint32_t nm = ctx->m;
@@ -864,8 +924,17 @@ int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* tar
             ctx->timing = ltg_timing{};
             upload_x(ctx, x, targets);
             clear_rare(ctx);
-            const bool ckpt = run_pass1(ctx, *cfg, plan, true, !cfg->fresh_step2_paths);
-            run_pass2(ctx, *cfg, plan, ckpt);
+            if (tangent) {
+                if (cfg->fresh_step2_paths) {
+                    run_pass1(ctx, *cfg, plan, true, false);
+                    run_tangent(ctx, *cfg, plan, false);
+                } else {
+                    run_tangent(ctx, *cfg, plan, true);
+                }
+            } else {
+                const bool ckpt = run_pass1(ctx, *cfg, plan, true, !cfg->fresh_step2_paths);
+                run_pass2(ctx, *cfg, plan, ckpt);
+            }
             st = ctx->stage(2 + 3 * nm + ctx->M);
             cuda_check(cudaMemcpyAsync(st, ctx->d_res.p, (1 + 3 * nm) * 8,
                                        cudaMemcpyDeviceToHost, ctx->stream),
@@ -892,6 +961,18 @@ int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* tar
         for (size_t j = 0; j < ctx->M; ++j) finite = finite && std::isfinite(report->grad[j]);
         if (!finite) throw Failure(LTG_ENUMERIC, "gradient_of_G: non-finite result");
     });
+}
+
+}  // namespace
+
+int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets, size_t m,
+                      const ltg_mc_config* cfg, ltg_report* report) {
+    return gradient_impl(ctx, x, M, targets, m, cfg, report, false);
+}
+
+int ltg_gradient_of_G_tangent(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
+                              size_t m, const ltg_mc_config* cfg, ltg_report* report) {
+    return gradient_impl(ctx, x, M, targets, m, cfg, report, true);
 }
 
 int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg,

@@ -119,6 +119,16 @@ __global__ void inverse_normal_kernel(const RngTables* tables, RngConsts rc, con
     z[i] = fabs(q) <= rc.lit_qmax ? as241_central(q, rc) : as241_tail(q, sh, rc);
 }
 
+// tangent mode: grad[d] = (sum_i lambda_i * J[i*M + d]) / P, i ascending
+__global__ void finalize_grad_tangent_kernel(const double* J, const double* lambda, uint32_t m,
+                                             uint32_t M, uint64_t paths, double* grad) {
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= M) return;
+    double t = 0.0;
+    for (uint32_t i = 0; i < m; ++i) t = __dadd_rn(t, __dmul_rn(lambda[i], J[(size_t)i * M + d]));
+    grad[d] = __ddiv_rn(t, (double)paths);
+}
+
 }  // namespace
 
 cudaError_t launch_reduce_chunks(const double* table, uint64_t n_chunks, uint32_t width,
@@ -156,6 +166,13 @@ cudaError_t launch_inverse_normal(const RngTables* tables, const RngConsts& rc, 
                                    uint64_t n, double* z, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     inverse_normal_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(tables, rc, p, n, z);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_grad_tangent(const double* J, const double* lambda, uint32_t m,
+                                         uint32_t M, uint64_t paths, double* grad,
+                                         cudaStream_t s) {
+    finalize_grad_tangent_kernel<<<(M + 127) / 128, 128, 0, s>>>(J, lambda, m, M, paths, grad);
     return cudaGetLastError();
 }
 

@@ -56,6 +56,7 @@ def load_library(path: str = LIB_PATH):
     L.ltg_pack_params.argtypes = [C.c_void_p, _dp, C.c_size_t]
     L.ltg_gradient_of_G.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, C.c_size_t,
                                     C.POINTER(MCConfigC), C.POINTER(ReportC)]
+    L.ltg_gradient_of_G_tangent.argtypes = L.ltg_gradient_of_G.argtypes
     L.ltg_estimate_means.argtypes = [C.c_void_p, _dp, C.c_size_t, C.POINTER(MCConfigC), _dp, _dp]
     L.ltg_finite_diff_gradient_of_G.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, C.c_size_t,
                                                 C.POINTER(MCConfigC), C.c_double, _dp]
@@ -169,15 +170,20 @@ class Engine:
         self.lib.ltg_pack_params(self.h, _p(x), self.M)
         return x
 
-    def gradient_of_G(self, x, targets, cfg: MCConfig, std_errors: bool = False) -> GradientReport:
-        """expectation.hpp:346-351"""
+    def gradient_of_G(self, x, targets, cfg: MCConfig, std_errors: bool = False,
+                      method: str = "adjoint") -> GradientReport:
+        """expectation.hpp:346-351. method="adjoint" is the reference's two-pass
+        scheme; "tangent" replaces pass 2 by pathwise forward tangents
+        (ltg_gradient_of_G_tangent: small-M Heston models only)."""
         xa, ta = _arr(x), _arr(targets)
         means, lam, grad = np.empty(self.m), np.empty(self.m), np.empty(self.M)
         se = np.empty(self.m) if std_errors else None
         rep = ReportC(0.0, _p(means), _p(lam), _p(grad), _p(se), 0, 0, 0)
         c = _cfg(cfg)
-        rc = self.lib.ltg_gradient_of_G(self.h, _p(xa), xa.size, _p(ta), ta.size, C.byref(c),
-                                        C.byref(rep))
+        if method not in ("adjoint", "tangent"):
+            raise ValueError(f"unknown method {method!r}")
+        fn = self.lib.ltg_gradient_of_G if method == "adjoint" else self.lib.ltg_gradient_of_G_tangent
+        rc = fn(self.h, _p(xa), xa.size, _p(ta), ta.size, C.byref(c), C.byref(rep))
         if rc:
             self._raise(rc)
         out = GradientReport(rep.G, means.tolist(), lam.tolist(), grad.tolist(), int(rep.paths),

@@ -308,6 +308,76 @@ def test_nccl_attached_single_rank_bitwise():
     assert eng.gradient_of_G(c.x, t, cfg).to_json() == base.to_json()
 
 
+# ------------------------------------------- tangent-mode alternative ----
+
+@pytest.mark.parametrize("name,paths,anti,fresh", [("cfg3", 4099, False, False),
+                                                  ("cfg3", 2048, True, False),
+                                                  ("cfg3", 3001, False, True),
+                                                  ("cfg1", 1 << 14, False, False),
+                                                  ("cfg1", 5000, True, True)])
+def test_tangent_mode_matches_reference(ref, name, paths, anti, fresh):
+    # pathwise tangents instead of pass 2: the reference's estimator on the
+    # same paths (grad = sum_i lambda_i J_i / P), so the same 1e-10 bar against
+    # the reference's two-pass gradient_of_G; G, means and lambda come from
+    # the same forward and are pass 1's bit for bit
+    c = configs.ALL[name]()
+    eng = Engine(c.spec)
+    prog = ref.program(c.spec)
+    t = configs.load_targets(c) or _targets_from(prog, c.truth, paths, 4242)
+    cfg = MCConfig(paths=paths, seed=c.seed, antithetic=anti, fresh_step2_paths=fresh)
+    orc = prog.gradient_of_G(c.x, t, paths, c.seed, antithetic=anti, fresh=fresh, workers=8)
+    rep = eng.gradient_of_G(c.x, t, cfg, method="tangent")
+    assert_report_close(rep, orc)
+    adj = eng.gradient_of_G(c.x, t, cfg)
+    assert rep.G == adj.G and rep.means == adj.means and rep.lambda_ == adj.lambda_
+    assert rel_err(rep.grad, adj.grad) <= 1e-12
+
+
+@pytest.mark.parametrize("env", [{"LTG_SAFE": "1"}])
+def test_tangent_mode_safe_rerun_bitwise(env):
+    import os
+    c = configs.cfg3()
+    eng = Engine(c.spec)
+    cfg = MCConfig(paths=3000, seed=c.seed)
+    t = configs.load_targets(c)
+    base = eng.gradient_of_G(c.x, t, cfg, method="tangent")
+    os.environ.update(env)
+    try:
+        rep = eng.gradient_of_G(c.x, t, cfg, method="tangent")
+    finally:
+        for k in env:
+            os.environ.pop(k)
+    assert rep.to_json() == base.to_json()
+
+
+def test_tangent_mode_nccl_attached_bitwise():
+    from paper_1901_04200_b200.engine import nccl_unique_id
+    c = configs.cfg3()
+    t = configs.load_targets(c)
+    cfg = MCConfig(paths=4099, seed=c.seed)
+    base = Engine(c.spec).gradient_of_G(c.x, t, cfg, method="tangent")
+    eng = Engine(c.spec)
+    eng.attach_nccl(nccl_unique_id(), 0, 1)
+    assert eng.gradient_of_G(c.x, t, cfg, method="tangent").to_json() == base.to_json()
+
+
+def test_tangent_mode_scope(small):
+    # grids with several leverage columns (heston_small, cfg2), the basket and
+    # fp32 are adjoint-only: refused where the reference would not be matched
+    spec, eng = small
+    x = eng.pack_params()
+    with pytest.raises(ValueError, match="tangent"):
+        eng.gradient_of_G(x, [1.0] * eng.m, MCConfig(paths=64, seed=1), method="tangent")
+    c = configs.cfg4()
+    with pytest.raises(ValueError, match="tangent"):
+        Engine(c.spec).gradient_of_G(c.x, c.targets, MCConfig(paths=64, seed=1),
+                                     method="tangent")
+    c = configs.cfg3()
+    with pytest.raises(ValueError, match="tangent"):
+        Engine(c.spec).gradient_of_G(c.x, configs.load_targets(c),
+                                     MCConfig(paths=64, seed=1, precision=1), method="tangent")
+
+
 def test_lambda_zero_identity(small):
     # test_calibrate.cpp:201-221: targets = means at the truth, same seed
     spec, eng = small
