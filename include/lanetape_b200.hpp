@@ -156,9 +156,11 @@ public:
     bool rng_exact() const { return ltg_rng_exact(ctx_) != 0; }
     ltg_ctx* handle() const { return ctx_; }
 
-    // expectation.hpp:346-351
+    // expectation.hpp:346-351. Method::tangent replaces pass 2 by pathwise
+    // forward tangents (ltg_gradient_of_G_tangent; small-M Heston models).
+    enum class Method { adjoint, tangent };
     GradientReport gradient_of_G(std::span<const double> x, std::span<const double> targets,
-                                 const MCConfig& cfg) const {
+                                 const MCConfig& cfg, Method method = Method::adjoint) const {
         GradientReport r;
         r.means.resize(num_outputs());
         r.lambda.resize(num_outputs());
@@ -168,8 +170,8 @@ public:
         rep.lambda = r.lambda.data();
         rep.grad = r.grad.data();
         const ltg_mc_config c = detail::to_c(cfg);
-        detail::check(ltg_gradient_of_G(ctx_, x.data(), x.size(), targets.data(), targets.size(),
-                                        &c, &rep),
+        auto* fn = method == Method::adjoint ? ltg_gradient_of_G : ltg_gradient_of_G_tangent;
+        detail::check(fn(ctx_, x.data(), x.size(), targets.data(), targets.size(), &c, &rep),
                       ltg_last_error(ctx_));
         r.G = rep.G;
         r.paths = rep.paths;
