@@ -297,8 +297,11 @@ def main():
                 "peak_source": "measured in this run: ltg_probe_fp64_rate (fastest of DFMA, "
                                "DMUL+DADD, DADD streams; 8 chains/thread, full occupancy)"}
         trf = census.dram_bytes_per_path(cfg.name, args.precision, dom)
-        if trf is not None:
-            roof["traffic"] = trf * paths_rank
+        if trf is not None and args.method == "adjoint":
+            # ncu bytes/path without the draw store (checkpoint table), plus
+            # the draw store this call wrote (pass 1) and read back (pass 2):
+            # pass 2 with draws measures 1,527 + 756*16 B/path (r1_v9_cfg3_full)
+            roof["traffic"] = trf * paths_rank + tm["z_bytes"]
         M, m = len(cfg.x), cfg.m
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
