@@ -122,11 +122,13 @@ __device__ inline void bflush(double* acc, uint32_t width, double* row, Map map)
 }
 
 // One forward path: S (and W when tracked); at every maturity event `visit`
-// is called with the event index.
-template <bool TRACK_W, typename Visit>
+// is called with the event index. SAFE = false uses glibc exp's main path
+// without the |x| >= 512 guard and raises the path's rare flag instead (the
+// host then reruns the call with SAFE = true; see heston.cu heston_step).
+template <bool TRACK_W, bool SAFE, typename Visit>
 __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, const Work& w,
                                          uint64_t base, bool neg, double (&S)[NA],
-                                         double (&W)[NA], Visit visit) {
+                                         double (&W)[NA], unsigned& chk, Visit visit) {
     const int tid = threadIdx.x, warp = tid >> 5;
     double* zb = s.zbuf + tid;
     uint16_t* wl = s.list + warp * 64 * BGS;
@@ -157,7 +159,16 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
                         wc = __dadd_rn(wc, __dmul_rn(a.chol[c * NA + b], z[b]));
                     if (TRACK_W) W[c] += wc;
                     const double x = __dadd_rn(a.drift[c], __dmul_rn(a.vol[c], wc));
-                    S[c] = __dmul_rn(S[c], exp_ref(x, s.tab->exp_tab, a.rc));
+                    double E;
+                    if (SAFE) {
+                        E = exp_ref(x, s.tab->exp_tab, a.rc);
+                    } else {
+                        // |x| >= 512 <=> (hi & 0x7ff00000) >= 0x40800000 (flag threshold
+                        // 0x7ca00000 after the shift, as in heston.cu)
+                        chk = max(chk, ((unsigned)__double2hiint(x) & 0x7ff00000u) + 0x3c200000u);
+                        E = a.rc.exact_exp ? glibc_exp_main(x, s.tab->exp_tab, a.rc) : exp(x);
+                    }
+                    S[c] = __dmul_rn(S[c], E);
                 }
             }
             if (k + 1 == ev_step) {
@@ -169,6 +180,9 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
     }
 }
 
+constexpr unsigned kBRareThr = 0x7ca00000u;
+
+template <bool SAFE>
 __global__ void __launch_bounds__(kBlock, 4) basket_pass1_kernel(BasketArgs a, Work w) {
     extern __shared__ __align__(16) char smem_raw[];
     __shared__ uint32_t chunk_slot;
@@ -187,6 +201,7 @@ __global__ void __launch_bounds__(kBlock, 4) basket_pass1_kernel(BasketArgs a, W
             const uint64_t base = w.antithetic ? path >> 1 : path;
             const bool neg = w.antithetic && (path & 1u);
             double S[NA], W[NA];
+            unsigned chk = 0;
             auto visit = [&](uint32_t ev, uint32_t ms) {
                 const MaturityEvent e = a.events[ev];
                 if (a.write_store && valid) {
@@ -213,9 +228,10 @@ __global__ void __launch_bounds__(kBlock, 4) basket_pass1_kernel(BasketArgs a, W
                 }
             };
             if (a.write_store)
-                simulate<true>(a, s, w, base, neg, S, W, visit);
+                simulate<true, SAFE>(a, s, w, base, neg, S, W, chk, visit);
             else
-                simulate<false>(a, s, w, base, neg, S, W, visit);
+                simulate<false, SAFE>(a, s, w, base, neg, S, W, chk, visit);
+            if (chk >= kBRareThr && valid) atomicOr(a.rare, 1u);
         }
         if (a.write_sums) {
             double* row = a.partials + ci * width;
@@ -238,6 +254,7 @@ __device__ __forceinline__ double contribution(const BasketArgs& a, const BSmem&
     return lam * Sa * (a.sqdt * Wa - a.sigma[c] * a.dt * (double)ms);
 }
 
+template <bool SAFE>
 __global__ void __launch_bounds__(kBlock, 4) basket_pass2_kernel(BasketArgs a, Work w) {
     extern __shared__ __align__(16) char smem_raw[];
     __shared__ uint32_t chunk_slot;
@@ -272,13 +289,16 @@ __global__ void __launch_bounds__(kBlock, 4) basket_pass2_kernel(BasketArgs a, W
                 const uint64_t base = w.antithetic ? path >> 1 : path;
                 const bool neg = w.antithetic && (path & 1u);
                 double S[NA], W[NA];
-                simulate<true>(a, s, w, base, neg, S, W, [&](uint32_t ev, uint32_t ms) {
+                unsigned chk = 0;
+                simulate<true, SAFE>(a, s, w, base, neg, S, W, chk,
+                                     [&](uint32_t ev, uint32_t ms) {
                     const MaturityEvent e = a.events[ev];
                     for (uint32_t pos = e.begin; pos < e.end; ++pos) {
                         const uint32_t c = (uint32_t)s.asset[pos];
                         add(pos, contribution(a, s, pos, ms, pick(S, c), pick(W, c)));
                     }
                 });
+                if (chk >= kBRareThr && valid) atomicOr(a.rare, 1u);
             }
         }
         double* row = a.partials + ci * width;
@@ -308,11 +328,15 @@ cudaError_t blaunch(K kernel, const BasketArgs& a, const Work& w, int grid, size
 }  // namespace
 
 cudaError_t launch_basket_pass1(const BasketArgs& a, const Work& w, int grid, cudaStream_t st) {
-    return blaunch(basket_pass1_kernel, a, w, grid, basket_smem(a.m, 2 * a.m), st);
+    const size_t smem = basket_smem(a.m, 2 * a.m);
+    return a.safe ? blaunch(basket_pass1_kernel<true>, a, w, grid, smem, st)
+                  : blaunch(basket_pass1_kernel<false>, a, w, grid, smem, st);
 }
 
 cudaError_t launch_basket_pass2(const BasketArgs& a, const Work& w, int grid, cudaStream_t st) {
-    return blaunch(basket_pass2_kernel, a, w, grid, basket_smem(a.m, a.n), st);
+    const size_t smem = basket_smem(a.m, a.n);
+    return a.safe ? blaunch(basket_pass2_kernel<true>, a, w, grid, smem, st)
+                  : blaunch(basket_pass2_kernel<false>, a, w, grid, smem, st);
 }
 
 }  // namespace ltg

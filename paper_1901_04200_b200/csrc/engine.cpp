@@ -316,6 +316,8 @@ BasketArgs basket_args(ltg_ctx* c, const double* x) {
     a.kind = c->d_kind.as<int32_t>();
     a.tables = c->d_tab.as<RngTables>();
     a.rc = c->h_rc;
+    a.safe = c->safe;
+    a.rare = c->d_counter.as<uint32_t>() + kRareSlot;
     return a;
 }
 

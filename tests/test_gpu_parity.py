@@ -308,6 +308,23 @@ def test_nccl_attached_single_rank_bitwise():
     assert eng.gradient_of_G(c.x, t, cfg).to_json() == base.to_json()
 
 
+@pytest.mark.parametrize("fresh", [False, True])
+def test_basket_safe_rerun_bitwise(fresh):
+    # the basket's fast exp path (rare flag instead of the |x| >= 512 guard)
+    # against the always-exact kernels, store and recompute pass 2
+    import os
+    c = configs.cfg4()
+    eng = Engine(c.spec)
+    cfg = MCConfig(paths=3001, seed=c.seed, fresh_step2_paths=fresh)
+    base = eng.gradient_of_G(c.x, c.targets, cfg)
+    os.environ["LTG_SAFE"] = "1"
+    try:
+        rep = eng.gradient_of_G(c.x, c.targets, cfg)
+    finally:
+        os.environ.pop("LTG_SAFE")
+    assert rep.to_json() == base.to_json()
+
+
 # ------------------------------------------- tangent-mode alternative ----
 
 @pytest.mark.parametrize("name,paths,anti,fresh", [("cfg3", 4099, False, False),
