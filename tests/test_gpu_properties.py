@@ -1,0 +1,117 @@
+"""Size-independent properties of the GPU engine at the BASELINE sizes.
+
+The reference's model tests (test_heston.cpp:188-252: martingale, put-call
+parity, Black-Scholes limit) restated where the oracle cannot follow: at 2^24
+and 2^26 paths on the device, on the config-5 Heston model. Put-call parity
+is an exact per-path identity (checked bit for bit), so its means agree to
+summation rounding; the martingale and BS limits are statistical and use the
+reference's standard-error formula (expectation.hpp:251-269) with a 5-SE band
+on fixed seeds.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1901_04200_b200 import configs
+from paper_1901_04200_b200.engine import Engine
+from paper_1901_04200_b200.model import (CALL, PUT, HestonParams, Instrument, LeverageGrid,
+                                         McSettings, MCConfig, ModelSpec)
+
+pytestmark = pytest.mark.gpu
+
+MATS = [63, 378, 756]
+K = 100.0
+
+
+def _parity_spec(paths):
+    # config 5's Heston model; per maturity: call K, put K, and S itself (a call
+    # struck at 1e-300: S - 1e-300 rounds to S, and strikes must be positive)
+    base = configs._heston_spec(paths)
+    ins = []
+    for ms in MATS:
+        ins += [Instrument(CALL, K, ms), Instrument(PUT, K, ms), Instrument(CALL, 1e-300, ms)]
+    return ModelSpec(base.heston, base.grid, ins, base.mc)
+
+
+@pytest.fixture(scope="module")
+def parity():
+    spec = _parity_spec(1 << 26)
+    eng = Engine(spec)
+    x = configs.cfg3().x
+    return spec, eng, x
+
+
+def test_put_call_parity_per_path_bitwise(parity):
+    # max(S-K,0) - max(K-S,0) == S - K exactly, path by path
+    spec, eng, x = parity
+    y = eng.path_payoffs(x, configs.GRAD_SEED, False, (1 << 26) - 4096, 4096)
+    for e in range(len(MATS)):
+        c, p, s = y[:, 3 * e], y[:, 3 * e + 1], y[:, 3 * e + 2]
+        assert np.array_equal(c - p, s - K)
+        assert np.all(s > 0.0)
+
+
+def test_put_call_parity_and_martingale_full_size(parity):
+    # 2^26 paths (config 5): mean(call) - mean(put) = mean(S) - K up to the
+    # rounding of two fixed-order sums; E[S_T] = S0 exp(mu T) (log-Euler is a
+    # martingale step by step) within 5 standard errors
+    spec, eng, x = parity
+    res = eng.estimate_means(x, MCConfig(paths=1 << 26, seed=configs.GRAD_SEED))
+    mu, s0, dt = spec.heston.mu, spec.heston.s0, spec.mc.dt
+    for e, ms in enumerate(MATS):
+        mc, mp, mS = res.means[3 * e], res.means[3 * e + 1], res.means[3 * e + 2]
+        assert abs((mc - mp) - (mS - K)) <= 1e-12 * mS
+        fwd = s0 * math.exp(mu * ms * dt)
+        se = res.std_errors[3 * e + 2]
+        assert 0.0 < se < 0.02
+        assert abs(mS - fwd) <= 5.0 * se, (ms, mS, fwd, se)
+
+
+def test_black_scholes_limit():
+    # V == 1 embedding with one flat leverage cell: log-Euler GBM is exact in
+    # distribution, so every undiscounted call mean matches Black-Scholes
+    # within 5 SE at 2^24 paths (acceptance.cpp:308-333 at 2^20)
+    sigma, mu, steps, dt = 0.25, 0.02, 64, 1.0 / 64
+    strikes = [70.0, 90.0, 100.0, 110.0, 140.0]
+    mats = [16, 64]
+    ins = [Instrument(CALL, k, ms) for ms in mats for k in strikes]
+    hp = HestonParams(mu=mu, kappa=0.0, theta=1.0, xi=0.0, rho=0.0, v0=1.0, s0=100.0)
+    spec = ModelSpec(hp, LeverageGrid([0.0], [0.0], [sigma]), ins,
+                     McSettings(1 << 24, steps, dt, 20190114))
+    eng = Engine(spec)
+    res = eng.estimate_means(eng.pack_params(), MCConfig(paths=1 << 24, seed=20190114))
+    for i, ins_i in enumerate(ins):
+        T = ins_i.maturity_step * dt
+        bs = configs.bs_call_undiscounted(100.0, ins_i.strike, sigma, T, mu)
+        assert abs(res.means[i] - bs) <= 5.0 * res.std_errors[i], (ins_i, res.means[i], bs)
+
+
+@pytest.fixture(scope="module")
+def cfg5():
+    c = configs.cfg5()
+    return c, Engine(c.spec)
+
+
+def test_lambda_zero_identity_full_size(cfg5):
+    # test_calibrate.cpp:201-221 at config 5's 2^26 paths: targets = the means
+    # of the same paths, so lambda == 0, G == 0 and grad == 0 exactly
+    c, eng = cfg5
+    cfg = MCConfig(paths=c.paths, seed=c.seed)
+    t = eng.estimate_means(c.x, cfg).means
+    rep = eng.gradient_of_G(c.x, t, cfg)
+    assert rep.G == 0.0 and all(v == 0.0 for v in rep.lambda_)
+    assert all(g == 0.0 for g in rep.grad)
+
+
+def test_adjoint_and_tangent_agree_full_size(cfg5):
+    # two algorithms, one estimator: the two-pass adjoint and the pathwise
+    # tangents on the same 2^26 paths
+    c, eng = cfg5
+    cfg = MCConfig(paths=c.paths, seed=c.seed)
+    t = configs.load_targets(c)
+    a = eng.gradient_of_G(c.x, t, cfg)
+    b = eng.gradient_of_G(c.x, t, cfg, method="tangent")
+    assert a.G == b.G and a.means == b.means
+    g1, g2 = np.asarray(a.grad), np.asarray(b.grad)
+    assert np.max(np.abs(g1 - g2) / np.maximum(np.abs(g1), 1e-12 * np.max(np.abs(g1)))) <= 1e-12
