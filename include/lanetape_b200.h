@@ -191,6 +191,16 @@ int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_con
 int ltg_finite_diff_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
                                   size_t m, const ltg_mc_config* cfg, double h, double* grad);
 
+/* One chunk of the two passes, unreduced (SURVEY §8(c) per-chunk parity):
+ * over the global paths [path0, path0+npaths) of PhiloxNormalSource(seed),
+ * the pass-1 sums Σy, Σy² (detail::forward_pass, expectation.hpp:152-198) and
+ * the pass-2 parameter-adjoint total seeded with the caller's lambda
+ * (detail::reverse_pass, :204-249) — the totals before the division by P.
+ * sums/sumsq: m, adjoint: M. Diagnostic / parity entry point. */
+int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda, size_t m,
+                   uint64_t seed, int antithetic, uint64_t path0, uint64_t npaths,
+                   double* sums, double* sumsq, double* adjoint);
+
 /* PhiloxNormalSource(seed, dim, antithetic).fill(path) for paths
  * [path0, path0+npaths), generated on the GPU; out is npaths*dim, path-major. */
 int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, uint64_t path0,

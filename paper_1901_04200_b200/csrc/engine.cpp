@@ -141,6 +141,7 @@ uint64_t chunks_per_rank(const ltg_shard& s, int world) {
 
 struct ltg_ctx {
     int kind = 0;  // 0 Heston SLV, 1 basket
+    uint64_t path_base = 0;  // global index of path 0 of a call (ltg_chunk_sums; else 0)
     bool ready = false;  // device state initialised
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -373,7 +374,7 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
 Work base_work(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan) {
     Work w{};
     w.paths = cfg.paths;
-    w.path_offset = 0;
+    w.path_offset = c->path_base;
     w.chunk_paths = plan.chunk_paths;
     w.chunk_begin = plan.chunk_begin;
     w.n_chunks = plan.chunk_end - plan.chunk_begin;
@@ -558,7 +559,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         b.use_store = have_ckpt && !cfg.fresh_step2_paths ? 1 : 0;
         b.store = b.use_store ? c->d_ckpt.as<double2>() : nullptr;
         b.store_stride = w.ckpt_stride;
-        if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
+        if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
         zero_counter(c, 2);
         w.counter = c->d_counter.as<uint32_t>() + 2;
         cuda_check(launch_basket_pass2(b, w, 0, c->stream), "basket pass 2");
@@ -567,7 +568,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         if (!have_ckpt && nseg > 1) {
             // fresh_step2_paths or no room for a full checkpoint table: replay
             // the pass-2 path set in waves (checkpoint-only forward, then adjoint)
-            if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
+            if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
             size_t free_b = 0, total_b = 0;
             cudaMemGetInfo(&free_b, &total_b);
             const size_t per_chunk = size_t(nseg - 1) * plan.chunk_paths * (c->fp32 ? 8 : 16);
@@ -601,7 +602,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                 c->timing.launches += 2;
             }
         } else {
-            if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
+            if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
             a.ckpt = c->d_ckpt.as<double2>();
             a.ztab = c->d_ztab.p;
             a.z_chunks = c->z_chunks;
@@ -644,7 +645,7 @@ void run_tangent(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bo
     a.partials = c->d_part2.as<double>() + plan.chunk_begin * width;
     a.write_sums = sums ? 1 : 0;
     Work w = base_work(c, cfg, plan);
-    if (cfg.fresh_step2_paths) w.path_offset = cfg.paths;
+    if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
     zero_counter(c, 2);
     w.counter = c->d_counter.as<uint32_t>() + 2;
     cuda_check(cudaEventRecord(c->ev[sums ? 0 : 3], c->stream), "event");
@@ -975,6 +976,50 @@ int ltg_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* tar
 int ltg_gradient_of_G_tangent(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
                               size_t m, const ltg_mc_config* cfg, ltg_report* report) {
     return gradient_impl(ctx, x, M, targets, m, cfg, report, true);
+}
+
+int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda, size_t m,
+                   uint64_t seed, int antithetic, uint64_t path0, uint64_t npaths,
+                   double* sums, double* sumsq, double* adjoint) {
+    if (!ctx) return LTG_EINVAL;
+    return guarded(ctx, [&] {
+        require(x && lambda && sums && sumsq && adjoint, "null buffer");
+        require(M == ctx->M && m == ctx->m, "chunk_sums: size mismatch");
+        require(npaths > 0, "chunk_sums: paths must be > 0");
+        check_params(ctx, x);
+        ltg_mc_config cfg{npaths, seed, antithetic, 0, 0, LTG_FP64};
+        const ltg_shard plan = make_plan(npaths, 0, 1);
+        struct Reset {
+            ltg_ctx* c;
+            ~Reset() { c->path_base = 0; }
+        } reset{ctx};
+        for (ctx->safe = force_safe();; ctx->safe = 1) {
+            ctx->timing = ltg_timing{};
+            ctx->path_base = path0;
+            upload_x(ctx, x, nullptr);
+            clear_rare(ctx);
+            const bool ckpt = run_pass1(ctx, cfg, plan, false, true);
+            // pass 2 seeded with the caller's lambda instead of pass 1's
+            cuda_check(cudaMemcpyAsync(ctx->d_res.as<double>() + 1 + 2 * ctx->m, lambda, m * 8,
+                                       cudaMemcpyHostToDevice, ctx->stream),
+                       "H2D");
+            run_pass2(ctx, cfg, plan, ckpt);
+            double* st = ctx->stage(2 * m + M + 1);
+            cuda_check(cudaMemcpyAsync(st, ctx->d_tot1.p, 2 * m * 8, cudaMemcpyDeviceToHost,
+                                       ctx->stream),
+                       "D2H");
+            cuda_check(cudaMemcpyAsync(st + 2 * m, ctx->d_tot2.p, M * 8, cudaMemcpyDeviceToHost,
+                                       ctx->stream),
+                       "D2H");
+            if (!take_rare(ctx, st + 2 * m + M) || ctx->safe) {
+                std::memcpy(sums, st, m * 8);
+                std::memcpy(sumsq, st + m, m * 8);
+                std::memcpy(adjoint, st + 2 * m, M * 8);
+                break;
+            }
+        }
+        ctx->safe = 0;
+    });
 }
 
 int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg,

@@ -63,6 +63,8 @@ def load_library(path: str = LIB_PATH):
     L.ltg_fill_normals.argtypes = [C.c_void_p, C.c_uint64, C.c_size_t, C.c_int, C.c_uint64,
                                    C.c_uint64, _dp]
     L.ltg_inverse_normal.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp]
+    L.ltg_chunk_sums.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, C.c_size_t, C.c_uint64,
+                                 C.c_int, C.c_uint64, C.c_uint64, _dp, _dp, _dp]
     L.ltg_last_timing.argtypes = [C.c_void_p, C.POINTER(TimingC)]
     L.ltg_path_payoffs.argtypes = [C.c_void_p, _dp, C.c_size_t, C.c_uint64, C.c_int, C.c_uint64,
                                    C.c_uint64, _dp]
@@ -221,6 +223,18 @@ class Engine:
         if rc:
             self._raise(rc)
         return out
+
+    def chunk_sums(self, x, lam, seed: int, antithetic: bool, path0: int, npaths: int):
+        """(Σy, Σy², adjoint total) over global paths [path0, path0+npaths): one
+        chunk of forward_pass / reverse_pass (expectation.hpp:152-249) seeded
+        with the given lambda."""
+        xa, la = _arr(x), _arr(lam)
+        s1, s2, adj = np.empty(self.m), np.empty(self.m), np.empty(self.M)
+        rc = self.lib.ltg_chunk_sums(self.h, _p(xa), xa.size, _p(la), la.size, seed,
+                                     int(antithetic), path0, npaths, _p(s1), _p(s2), _p(adj))
+        if rc:
+            self._raise(rc)
+        return s1, s2, adj
 
     def inverse_normal(self, p) -> np.ndarray:
         """inverse_normal_cdf(p) elementwise on the GPU (rng.hpp:45-85); p of the

@@ -10,6 +10,7 @@ BASELINE.json):
     (tests/support/oracles.hpp:19-22 style rel_err).
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -455,3 +456,51 @@ def test_error_behaviour(small):
     bad[3] = 1.5  # rho: sqrt(1 - rho^2) of a negative -> EvalError in the reference
     with pytest.raises(EvalError):
         eng.gradient_of_G(bad, [1.0] * 4, MCConfig(paths=10, seed=1))
+
+
+# ------------------------------------- per-chunk parity at full P (§8c) ----
+
+def _chunk_lambda(m):
+    return np.array([0.05 * math.sin(1.0 + i) for i in range(m)])
+
+
+@pytest.mark.parametrize("k,anti", [(0, False), (517, False), (1023, False), (731, True)])
+def test_cfg5_chunk_sums_match_reference(ref, k, anti):
+    # 2^16-path chunks of config 5 at their place in the full
+    # 2^26 path set — the reference's forward_pass / reverse_pass on the same
+    # chunk (path_offset = k*2^16) against the GPU's unreduced chunk totals
+    c = configs.cfg5()
+    eng = Engine(c.spec)
+    prog = ref.program(c.spec)
+    lam = _chunk_lambda(c.m)
+    p0, n = k << 16, 1 << 16
+    s1, s2, adj = eng.chunk_sums(c.x, lam, c.seed, anti, p0, n)
+    r1, r2 = prog.forward_sums(c.x, c.seed, p0, n, antithetic=anti, workers=os.cpu_count())
+    radj = prog.reverse_sums(c.x, c.seed, p0, n, lam, antithetic=anti, workers=os.cpu_count())
+    assert rel_err(s1, r1, 1e-12) <= 1e-12
+    assert rel_err(s2, r2, 1e-12) <= 1e-12
+    assert rel_err(adj, radj) <= TOL, (adj, radj)
+
+
+def test_cfg4_chunk_sums_match_reference(ref):
+    c = configs.cfg4()
+    eng = Engine(c.spec)
+    prog = ref.program(c.spec)
+    lam = _chunk_lambda(c.m)
+    p0, n = 3 << 20, 1 << 14
+    s1, s2, adj = eng.chunk_sums(c.x, lam, c.seed, False, p0, n)
+    r1, r2 = prog.forward_sums(c.x, c.seed, p0, n, workers=os.cpu_count())
+    radj = prog.reverse_sums(c.x, c.seed, p0, n, lam, workers=os.cpu_count())
+    assert rel_err(s1, r1, 1e-12) <= 1e-12 and rel_err(s2, r2, 1e-12) <= 1e-12
+    assert rel_err(adj, radj) <= TOL
+
+
+def test_cfg5_end_to_end_2p22(ref):
+    # config 5's model end to end at P = 2^22 against the
+    # reference's gradient_of_G (all host cores; ~30 s of CPU)
+    c = configs.cfg5(1 << 22)
+    t = configs.load_targets(configs.cfg5())
+    prog = ref.program(c.spec)
+    orc = prog.gradient_of_G(c.x, t, c.paths, c.seed, workers=os.cpu_count())
+    rep = Engine(c.spec).gradient_of_G(c.x, t, MCConfig(paths=c.paths, seed=c.seed))
+    assert_report_close(rep, orc)
