@@ -166,7 +166,7 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
                         // |x| >= 512 <=> (hi & 0x7ff00000) >= 0x40800000 (flag threshold
                         // 0x7ca00000 after the shift, as in heston.cu)
                         chk = max(chk, ((unsigned)__double2hiint(x) & 0x7ff00000u) + 0x3c200000u);
-                        E = a.rc.exact_exp ? glibc_exp_main(x, s.tab->exp_tab, a.rc) : exp(x);
+                        E = glibc_exp_main(x, s.tab->exp_tab, a.rc);  // validated table
                     }
                     S[c] = __dmul_rn(S[c], E);
                 }

@@ -687,9 +687,13 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 // The fast arithmetic's out-of-range flag (heston.cu heston_step): cleared
 // before a call, OR-ed across ranks, copied back with the results. A set flag
 // makes the caller redo the call in safe mode.
-int force_safe() {  // LTG_SAFE=1: start in safe mode (tests)
+// Calls start in fast mode unless LTG_SAFE=1 (tests) or the host libm's exp
+// table could not be validated: the fast kernels use glibc's exp main path
+// unconditionally, so without an exact table every call runs the SAFE
+// kernels (which fall back to CUDA's exp).
+int start_safe(const ltg_ctx* c) {
     const char* e = std::getenv("LTG_SAFE");
-    return e && e[0] == '1' ? 1 : 0;
+    return (e && e[0] == '1') || !c->h_rc.exact_exp ? 1 : 0;
 }
 
 void clear_rare(ltg_ctx* c) {
@@ -923,7 +927,7 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
         const uint32_t nm = ctx->m;
         double* st = nullptr;
-        for (ctx->safe = force_safe();; ctx->safe = 1) {
+        for (ctx->safe = start_safe(ctx);; ctx->safe = 1) {
             ctx->timing = ltg_timing{};
             upload_x(ctx, x, targets);
             clear_rare(ctx);
@@ -993,7 +997,7 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
             ltg_ctx* c;
             ~Reset() { c->path_base = 0; }
         } reset{ctx};
-        for (ctx->safe = force_safe();; ctx->safe = 1) {
+        for (ctx->safe = start_safe(ctx);; ctx->safe = 1) {
             ctx->timing = ltg_timing{};
             ctx->path_base = path0;
             upload_x(ctx, x, nullptr);
@@ -1032,7 +1036,7 @@ int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_con
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
         const uint32_t nm = ctx->m;
         double* st = nullptr;
-        for (ctx->safe = force_safe();; ctx->safe = 1) {
+        for (ctx->safe = start_safe(ctx);; ctx->safe = 1) {
             ctx->timing = ltg_timing{};
             upload_x(ctx, x, nullptr);
             clear_rare(ctx);
