@@ -125,14 +125,14 @@ __device__ inline void bflush(double* acc, uint32_t width, double* row, Map map)
 // is called with the event index. SAFE = false uses glibc exp's main path
 // without the |x| >= 512 guard and raises the path's rare flag instead (the
 // host then reruns the call with SAFE = true; see heston.cu heston_step).
-template <bool TRACK_W, bool SAFE, typename Visit>
+template <bool TRACK_W, bool SAFE, int NAT, typename Visit>
 __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, const Work& w,
                                          uint64_t base, bool neg, double (&S)[NA],
                                          double (&W)[NA], unsigned& chk, Visit visit) {
     const int tid = threadIdx.x, warp = tid >> 5;
     double* zb = s.zbuf + tid;
     uint16_t* wl = s.list + warp * 64 * BGS;
-    const uint32_t n = a.n;
+    const uint32_t n = NAT ? (uint32_t)NAT : a.n;  // NAT: asset count fixed at compile time
 #pragma unroll
     for (int c = 0; c < NA; ++c) {
         S[c] = a.s0[c];
@@ -182,11 +182,12 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
 
 constexpr unsigned kBRareThr = 0x7ca00000u;
 
-template <bool SAFE>
+// NAT = 16 (config 4) specialises the asset loops; NAT = 0 takes a.n at run time
+template <bool SAFE, int NAT>
 __global__ void __launch_bounds__(kBlock, 4) basket_pass1_kernel(BasketArgs a, Work w) {
     extern __shared__ __align__(16) char smem_raw[];
     __shared__ uint32_t chunk_slot;
-    const uint32_t m = a.m, width = 2 * m, n = a.n;
+    const uint32_t m = a.m, width = 2 * m, n = NAT ? (uint32_t)NAT : a.n;
     const BSmem s = bcarve(smem_raw, m, width);
     bload(a, s, width, false);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -228,9 +229,9 @@ __global__ void __launch_bounds__(kBlock, 4) basket_pass1_kernel(BasketArgs a, W
                 }
             };
             if (a.write_store)
-                simulate<true, SAFE>(a, s, w, base, neg, S, W, chk, visit);
+                simulate<true, SAFE, NAT>(a, s, w, base, neg, S, W, chk, visit);
             else
-                simulate<false, SAFE>(a, s, w, base, neg, S, W, chk, visit);
+                simulate<false, SAFE, NAT>(a, s, w, base, neg, S, W, chk, visit);
             if (chk >= kBRareThr && valid) atomicOr(a.rare, 1u);
         }
         if (a.write_sums) {
@@ -254,11 +255,11 @@ __device__ __forceinline__ double contribution(const BasketArgs& a, const BSmem&
     return lam * Sa * (a.sqdt * Wa - a.sigma[c] * a.dt * (double)ms);
 }
 
-template <bool SAFE>
+template <bool SAFE, int NAT>
 __global__ void __launch_bounds__(kBlock, 4) basket_pass2_kernel(BasketArgs a, Work w) {
     extern __shared__ __align__(16) char smem_raw[];
     __shared__ uint32_t chunk_slot;
-    const uint32_t m = a.m, n = a.n, width = n;
+    const uint32_t m = a.m, n = NAT ? (uint32_t)NAT : a.n, width = n;
     const BSmem s = bcarve(smem_raw, m, width);
     bload(a, s, width, true);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kBlock, 4) basket_pass2_kernel(BasketArgs a, W
                 const bool neg = w.antithetic && (path & 1u);
                 double S[NA], W[NA];
                 unsigned chk = 0;
-                simulate<true, SAFE>(a, s, w, base, neg, S, W, chk,
+                simulate<true, SAFE, NAT>(a, s, w, base, neg, S, W, chk,
                                      [&](uint32_t ev, uint32_t ms) {
                     const MaturityEvent e = a.events[ev];
                     for (uint32_t pos = e.begin; pos < e.end; ++pos) {
@@ -329,14 +330,20 @@ cudaError_t blaunch(K kernel, const BasketArgs& a, const Work& w, int grid, size
 
 cudaError_t launch_basket_pass1(const BasketArgs& a, const Work& w, int grid, cudaStream_t st) {
     const size_t smem = basket_smem(a.m, 2 * a.m);
-    return a.safe ? blaunch(basket_pass1_kernel<true>, a, w, grid, smem, st)
-                  : blaunch(basket_pass1_kernel<false>, a, w, grid, smem, st);
+    if (a.n == kMaxAssets)
+        return a.safe ? blaunch(basket_pass1_kernel<true, kMaxAssets>, a, w, grid, smem, st)
+                      : blaunch(basket_pass1_kernel<false, kMaxAssets>, a, w, grid, smem, st);
+    return a.safe ? blaunch(basket_pass1_kernel<true, 0>, a, w, grid, smem, st)
+                  : blaunch(basket_pass1_kernel<false, 0>, a, w, grid, smem, st);
 }
 
 cudaError_t launch_basket_pass2(const BasketArgs& a, const Work& w, int grid, cudaStream_t st) {
     const size_t smem = basket_smem(a.m, a.n);
-    return a.safe ? blaunch(basket_pass2_kernel<true>, a, w, grid, smem, st)
-                  : blaunch(basket_pass2_kernel<false>, a, w, grid, smem, st);
+    if (a.n == kMaxAssets)
+        return a.safe ? blaunch(basket_pass2_kernel<true, kMaxAssets>, a, w, grid, smem, st)
+                      : blaunch(basket_pass2_kernel<false, kMaxAssets>, a, w, grid, smem, st);
+    return a.safe ? blaunch(basket_pass2_kernel<true, 0>, a, w, grid, smem, st)
+                  : blaunch(basket_pass2_kernel<false, 0>, a, w, grid, smem, st);
 }
 
 }  // namespace ltg
