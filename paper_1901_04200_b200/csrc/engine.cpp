@@ -461,7 +461,11 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         cudaMemGetInfo(&free_b, &total_b);
         const size_t reserve = size_t(2) << 30;
         const size_t held = c->d_ckpt.bytes + c->d_ztab.bytes;
-        const size_t avail = free_b + held > reserve ? free_b + held - reserve : 0;
+        size_t avail = free_b + held > reserve ? free_b + held - reserve : 0;
+        // LTG_HBM_BUDGET_GB caps checkpoint table + draw store (GPUs shared
+        // with other work); the default takes what is free
+        if (const char* cap = std::getenv("LTG_HBM_BUDGET_GB"))
+            avail = std::min<size_t>(avail, size_t(std::strtod(cap, nullptr) * double(1ull << 30)));
         const size_t elem = c->fp32 ? 8 : 16;
         const uint64_t nloc = w.n_chunks;
         const size_t z_chunk = size_t(c->steps) * plan.chunk_paths * elem;

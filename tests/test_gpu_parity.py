@@ -269,6 +269,7 @@ def test_fresh_step2_paths(ref, small):
 
 
 @pytest.mark.parametrize("env", [{"LTG_ZSTORE": "0"}, {"LTG_ZCHUNKS_MAX": "3"},
+                                 {"LTG_HBM_BUDGET_GB": "0.1"}, {"LTG_HBM_BUDGET_GB": "0"},
                                  {"LTG_CKPT_STEPS": "16"},
                                  {"LTG_CKPT_STEPS": "16", "LTG_ZSTORE": "0"},
                                  {"LTG_SAFE": "1"}])
