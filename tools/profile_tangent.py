@@ -7,5 +7,6 @@ from paper_1901_04200_b200.model import MCConfig
 c = configs.cfg3()
 eng = Engine(c.spec)
 t = configs.load_targets(c)
-rep = eng.gradient_of_G(c.x, t, MCConfig(paths=1 << 18, seed=c.seed), method="tangent")
+import os
+rep = eng.gradient_of_G(c.x, t, MCConfig(paths=int(os.environ.get("LTG_PATHS", 1 << 18)), seed=c.seed), method="tangent")
 print(json.dumps(eng.timing()))
