@@ -107,8 +107,12 @@ def cpu_reference_rate(cfg, targets, sample_paths, workers, reps=1):
 
 
 def size_cpu_sample(cfg, targets, workers, seconds):
+    """Sample size for `seconds` of the reference's CPU work: a 1024-path probe,
+    then a ~1 s probe (thread start-up makes the small one pessimistic)."""
     probe = 1024
     rate, _ = cpu_reference_rate(cfg, targets, probe, workers)
+    probe2 = max(probe, int(rate) // 1024 * 1024)
+    rate, _ = cpu_reference_rate(cfg, targets, probe2, workers)
     return max(probe, int(rate * seconds) // 1024 * 1024), rate
 
 
