@@ -163,7 +163,7 @@ def main():
     ap.add_argument("--config", default="cfg5", choices=sorted(configs.ALL))
     ap.add_argument("--paths", type=int, default=0, help="override the config's path count")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
-    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--ref-seconds", type=float, default=4.0,
                     help="target time of one --impl reference step")
