@@ -1,0 +1,53 @@
+"""bench.py's engine arm on the GPU: the JSON line the driver reads (keys,
+units, the roofline / cpu_baseline / e2e / clocks objects), on a small config
+so the check takes seconds."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    return lines[0]
+
+
+def test_engine_arm_json_contract():
+    d = _run("--config", "cfg3", "--paths", "65536", "--steps", "2", "--warmup", "3",
+             "--cpu-seconds", "0.5")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+              "gpu_launches", "clocks", "roofline", "cpu_baseline"):
+        assert k in d, k
+    assert d["metric"] == "grad_G_mc_paths_per_sec" and d["unit"] == "paths/s"
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3
+    assert d["dtype"] == "f64" and d["higher_is_better"] is True
+    assert d["config"]["workload"] == "cfg3_heston"
+    assert d["gpu_launches"] == 2 * 8                  # 8 kernels per gradient_of_G
+    e = d["e2e"]
+    assert e["unit"] == "paths/s" and 0 < e["value"] and e["h2d_bytes_per_step"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "fp64" and 0 < r["frac"] < 1.2 and r["peak"] > 1.0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["clocks"]["samples"] >= 0
+    assert "tangent" in d["alt_methods"]
+
+
+def test_engine_arm_fp32_and_tangent_method():
+    d = _run("--config", "cfg3", "--paths", "65536", "--steps", "1", "--warmup", "3",
+             "--no-cpu-baseline", "--precision", "fp32", "--no-alt-method")
+    assert d["dtype"] == "f32" and d["value"] > 0 and "alt_methods" not in d
+    t = _run("--config", "cfg3", "--paths", "65536", "--steps", "1", "--warmup", "3",
+             "--no-cpu-baseline", "--method", "tangent")
+    assert t["method"] == "tangent" and t["value"] > 0
