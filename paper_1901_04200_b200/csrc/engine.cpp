@@ -7,7 +7,12 @@
 //   fixed-order chunk reduction -> means, std errors, lambda, G   (all on device)
 //   pass 2  adjoint kernel over the same chunks          -> chunk partials
 //   [NCCL all-gather]  fixed-order reduction -> grad = total / P
-//   one device->host copy of {G, means, se, lambda, grad}
+//   one device->host copy of {G, means, se, lambda, grad} and the rare flag
+// The fast kernels flag arguments outside their exact range; a flagged call
+// (flag all-reduced over ranks) is rerun with the SAFE kernels, bit-identical
+// where both are defined. ltg_gradient_of_G_tangent replaces pass 2 by the
+// pathwise-tangent kernel (run_tangent); ltg_chunk_sums runs one global path
+// range of both passes unreduced (parity checks).
 // Validation mirrors the reference's std::invalid_argument sites; a non-finite
 // result maps to LTG_ENUMERIC like EvalError.
 #include <cuda_runtime.h>
