@@ -1222,6 +1222,8 @@ int ltg_attach_nccl(ltg_ctx* ctx, const unsigned char id[128], int rank, int wor
         std::memcpy(&u, id, 128);
         if (ctx->comm) nccl().CommDestroy(ctx->comm);
         ctx->comm = nullptr;
+        ctx->rank = 0;  // single-GPU until the new communicator exists
+        ctx->world = 1;
         const ncclResult_t r = nccl().CommInitRank(&ctx->comm, world, u, rank);
         if (r != ncclSuccess)
             throw Failure(LTG_ECUDA, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
