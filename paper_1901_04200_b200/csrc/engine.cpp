@@ -1224,9 +1224,11 @@ int ltg_attach_nccl(ltg_ctx* ctx, const unsigned char id[128], int rank, int wor
         ctx->comm = nullptr;
         ctx->rank = 0;  // single-GPU until the new communicator exists
         ctx->world = 1;
-        const ncclResult_t r = nccl().CommInitRank(&ctx->comm, world, u, rank);
+        ncclComm_t comm = nullptr;
+        const ncclResult_t r = nccl().CommInitRank(&comm, world, u, rank);
         if (r != ncclSuccess)
             throw Failure(LTG_ECUDA, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+        ctx->comm = comm;
         ctx->rank = rank;
         ctx->world = world;
     });
