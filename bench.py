@@ -190,7 +190,8 @@ def main():
             pg.destroy_process_group()
         return rc
 
-    from paper_1901_04200_b200.engine import Engine, nccl_unique_id, probe_fp64_rate
+    from paper_1901_04200_b200.engine import (Engine, nccl_unique_id, probe_fp32_rate,
+                                              probe_fp64_rate)
 
     cfg = build_cfg(args.config, args.paths)
     targets = configs.load_targets(cfg)
@@ -275,31 +276,37 @@ def main():
         K = args.steps
         value = cfg.paths * K / (dev_total * 1e-3)
         e2e = cfg.paths * K / wall
-        peak = probe_fp64_rate(local)
-        # dominant kernel of the step (device time), its frozen FP64 census
+        fp32 = args.precision == "fp32"
+        # fp64: FP64 issue; fp32 mode: its FP32 arithmetic against the FFMA rate
+        peak = probe_fp32_rate(local) if fp32 else probe_fp64_rate(local)
+        # dominant kernel of the step (device time), its frozen census
         dom = "pass2" if p2_tot >= p1_tot else "pass1"
         basket = not hasattr(cfg.spec, "mc")
         kname = ("basket_" if basket else "heston_") + dom + "_kernel"
-        w = (census.pass2_fp64_per_path if dom == "pass2" else census.pass1_fp64_per_path)(
-            cfg.name, args.precision)
+        if fp32:
+            w1, w2 = census.pass1_fp32_per_path, census.pass2_fp32_per_path
+        else:
+            w1, w2 = census.pass1_fp64_per_path, census.pass2_fp64_per_path
+        w = (w2 if dom == "pass2" else w1)(cfg.name, args.precision)
         if args.method == "tangent":  # one forward+tangent kernel; no frozen census
             kname, w = "heston_tangent_kernel", None
         paths_rank = tm["paths_pass2"] if dom == "pass2" else tm["paths_pass1"]
         t_dom = (p2_tot if dom == "pass2" else p1_tot) / K * 1e-3
         achieved = (w * paths_rank / t_dom) if w else None
-        w_all = [census.pass1_fp64_per_path(cfg.name, args.precision),
-                 census.pass2_fp64_per_path(cfg.name, args.precision)]
+        w_all = [w1(cfg.name, args.precision), w2(cfg.name, args.precision)]
         if args.method == "tangent":
             w_all = [None]
-        roof = {"bound": "fp64", "kernel": kname,
+        roof = {"bound": "fp32" if fp32 else "fp64", "kernel": kname,
                 "achieved": achieved / 1e12 if achieved else None,
-                "peak": peak / 1e12, "unit": "T fp64-inst/s",
+                "peak": peak / 1e12, "unit": "T fp32-inst/s" if fp32 else "T fp64-inst/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
-                "census_fp64_per_path": w,
+                "census_inst_per_path": w,
                 "whole_step_frac": (sum(w_all) * cfg.paths * K / (dev_total * 1e-3) / peak)
                 if all(w_all) else None,
-                "peak_source": "measured in this run: ltg_probe_fp64_rate (fastest of DFMA, "
-                               "DMUL+DADD, DADD streams; 8 chains/thread, full occupancy)"}
+                "peak_source": ("measured in this run: ltg_probe_fp32_rate (FFMA streams; 8 "
+                                "chains/thread, full occupancy)") if fp32 else
+                               ("measured in this run: ltg_probe_fp64_rate (fastest of DFMA, "
+                                "DMUL+DADD, DADD streams; 8 chains/thread, full occupancy)")}
         trf = census.dram_bytes_per_path(cfg.name, args.precision, dom)
         if trf is not None and args.method == "adjoint":
             # ncu bytes/path without the draw store (checkpoint table), plus

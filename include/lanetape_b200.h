@@ -241,6 +241,9 @@ int ltg_attach_nccl(ltg_ctx* ctx, const unsigned char id[128], int rank, int wor
  * (8 independent chains per thread, full occupancy, best of 3) — the
  * roofline denominator reported by bench.py. */
 int ltg_probe_fp64_rate(int device, double* fp64_per_s, double* sm_clock_hz);
+/* Diagnostic: measured FP32 FFMA issue rate (thread instructions per second,
+ * 8 chains per thread, full occupancy) — the fp32 mode's roofline denominator. */
+int ltg_probe_fp32_rate(int device, double* fp32_per_s);
 
 /* Host-only self-test of the random stream's log(): locates and validates
  * the host libm table (as context creation does) and compares the GPU's

@@ -23,6 +23,12 @@ PASS1_FP64 = {"cfg3_heston:fp64": 107979.0, "cfg1_gbm:fp64": 2394.0,
               "cfg2_localvol:fp64": 9945.0, "cfg4_basket16:fp64": 67307.0}
 PASS2_FP64 = {"cfg3_heston:fp64": 143004.0, "cfg1_gbm:fp64": 2960.0,
               "cfg2_localvol:fp64": 12346.0, "cfg4_basket16:fp64": 503.0}
+# fp32 mode: thread-level FADD + FFMA + FMUL per path (the arithmetic the FP32
+# pipe executes), counted without the draw store on the r1 kernels (cfg3 fp32
+# at 2^18, LTG_ZSTORE=0); the mode also keeps ~6-7k FP64 instructions per pass
+# (the exact uniform and tail arguments) and all of Philox
+PASS1_FP32 = {"cfg3_heston:fp32": 45249.3}
+PASS2_FP32 = {"cfg3_heston:fp32": 67958.8}
 # per-path DRAM bytes (ncu dram__bytes_read+write / paths), latest capture without the
 # draw store (profiles/r1_v9_cfg3_noz_full.txt: the regime of cfg5 on one GPU)
 PASS1_DRAM = {"cfg3_heston:fp64": 1457.1}
@@ -55,3 +61,11 @@ def ckpt_bytes(cfg) -> float:
         return 0.0
     nseg = (spec.mc.steps + SEG_STEPS - 1) // SEG_STEPS
     return float(max(0, nseg - 1)) * cfg.paths * 16
+
+
+def pass1_fp32_per_path(name: str, precision: str = "fp32"):
+    return PASS1_FP32.get(_key(name, precision))
+
+
+def pass2_fp32_per_path(name: str, precision: str = "fp32"):
+    return PASS2_FP32.get(_key(name, precision))

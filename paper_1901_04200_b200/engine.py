@@ -73,6 +73,7 @@ def load_library(path: str = LIB_PATH):
     L.ltg_nccl_unique_id.argtypes = [C.c_char_p]
     L.ltg_attach_nccl.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int]
     L.ltg_probe_fp64_rate.argtypes = [C.c_int, _dp, _dp]
+    L.ltg_probe_fp32_rate.argtypes = [C.c_int, _dp]
     L.ltg_rng_selftest.argtypes = [C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]
     _lib = L
     return L
@@ -84,6 +85,15 @@ def probe_fp64_rate(device: int = 0) -> float:
     r, clk = C.c_double(), C.c_double()
     if L.ltg_probe_fp64_rate(device, C.byref(r), C.byref(clk)):
         raise EngineError("fp64 probe failed")
+    return r.value
+
+
+def probe_fp32_rate(device: int = 0) -> float:
+    """Measured FP32 FFMA issue rate (thread instructions/s) of the GPU."""
+    L = load_library()
+    r = C.c_double()
+    if L.ltg_probe_fp32_rate(device, C.byref(r)):
+        raise EngineError("fp32 probe failed")
     return r.value
 
 

@@ -48,6 +48,7 @@ def test_engine_arm_fp32_and_tangent_method():
     d = _run("--config", "cfg3", "--paths", "65536", "--steps", "1", "--warmup", "3",
              "--no-cpu-baseline", "--precision", "fp32", "--no-alt-method")
     assert d["dtype"] == "f32" and d["value"] > 0 and "alt_methods" not in d
+    assert d["roofline"]["bound"] == "fp32" and 0 < d["roofline"]["frac"] < 1.2
     t = _run("--config", "cfg3", "--paths", "65536", "--steps", "1", "--warmup", "3",
              "--no-cpu-baseline", "--method", "tangent")
     assert t["method"] == "tangent" and t["value"] > 0
