@@ -19,22 +19,10 @@
 
 #include "lanetape/lanetape.hpp"
 #include "lanetape_b200.hpp"
+#include "lanetape_b200_ref.hpp"
 
 namespace lt = lanetape;
 namespace gpu = lanetape_b200;
-
-static gpu::ModelSpec to_gpu(const lt::ModelSpec& s) {
-    gpu::ModelSpec g;
-    g.heston = {s.heston.mu, s.heston.kappa, s.heston.theta, s.heston.xi,
-                s.heston.rho, s.heston.v0,   s.heston.s0};
-    g.grid = {s.grid.t_nodes, s.grid.s_nodes, s.grid.values};
-    for (const auto& i : s.instruments)
-        g.instruments.push_back({i.kind == lt::Instrument::Kind::Put ? gpu::Instrument::Kind::Put
-                                                                     : gpu::Instrument::Kind::Call,
-                                 i.strike, i.maturity_step});
-    g.mc = {s.mc.paths, s.mc.steps, s.mc.dt, s.mc.seed};
-    return g;
-}
 
 int main(int argc, char** argv) {
     if (argc < 2) {
@@ -45,7 +33,7 @@ int main(int argc, char** argv) {
         const auto t0 = std::chrono::steady_clock::now();
         const lt::ModelSpec spec = lt::load_model_spec(argv[1]);
         const std::vector<double> truth = lt::pack_params(spec.heston, spec.grid);
-        gpu::Engine engine(to_gpu(spec));
+        gpu::Engine engine(gpu::to_gpu(spec));
         gpu::MCConfig cfg;
         cfg.paths = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : spec.mc.paths;
         cfg.seed = spec.mc.seed;

@@ -32,6 +32,7 @@
 
 #include "lanetape/lanetape.hpp"
 #include "lanetape_b200.hpp"
+#include "lanetape_b200_ref.hpp"
 
 namespace lt = lanetape;
 namespace gpu = lanetape_b200;
@@ -97,19 +98,6 @@ Opts parse(int argc, char** argv) {
     return o;
 }
 
-gpu::ModelSpec to_gpu(const lt::ModelSpec& s) {
-    gpu::ModelSpec g;
-    g.heston = {s.heston.mu, s.heston.kappa, s.heston.theta, s.heston.xi,
-                s.heston.rho, s.heston.v0,   s.heston.s0};
-    g.grid = {s.grid.t_nodes, s.grid.s_nodes, s.grid.values};
-    for (const auto& i : s.instruments)
-        g.instruments.push_back({i.kind == lt::Instrument::Kind::Put ? gpu::Instrument::Kind::Put
-                                                                     : gpu::Instrument::Kind::Call,
-                                 i.strike, i.maturity_step});
-    g.mc = {s.mc.paths, s.mc.steps, s.mc.dt, s.mc.seed};
-    return g;
-}
-
 // main.cpp:72-81
 nlohmann::ordered_json effective_config(const Opts& o, const lt::ModelSpec& spec) {
     nlohmann::ordered_json j;
@@ -152,7 +140,7 @@ gpu::MCConfig mc_config(const lt::ModelSpec& spec, const Opts& o) {
 }
 
 int run_price(const Opts& o, const lt::ModelSpec& spec) {
-    gpu::Engine engine(to_gpu(spec));
+    gpu::Engine engine(gpu::to_gpu(spec));
     const std::vector<double> x = lt::pack_params(spec.heston, spec.grid);
     const auto means = engine.estimate_means(x, mc_config(spec, o));
     require_finite(means.means, "price means");
@@ -170,7 +158,7 @@ int run_price(const Opts& o, const lt::ModelSpec& spec) {
 
 // main.cpp:134-182: targets are 90% of the means at the config parameters
 int run_gradcheck(const Opts& o, const lt::ModelSpec& spec) {
-    gpu::Engine engine(to_gpu(spec));
+    gpu::Engine engine(gpu::to_gpu(spec));
     const gpu::MCConfig cfg = mc_config(spec, o);
     const std::vector<double> x = lt::pack_params(spec.heston, spec.grid);
     const auto means = engine.estimate_means(x, cfg);
@@ -232,7 +220,7 @@ std::vector<std::string> split_csv(const std::string& s) {
 // main.cpp:256-382: gradient_descent (unchanged, the reference's) on synthetic
 // targets at the truth, descending in truth-scaled coordinates
 int run_calibrate(const Opts& o, const lt::ModelSpec& spec) {
-    gpu::Engine engine(to_gpu(spec));
+    gpu::Engine engine(gpu::to_gpu(spec));
     const gpu::MCConfig cfg = mc_config(spec, o);
     const std::vector<double> truth = lt::pack_params(spec.heston, spec.grid);
     const std::size_t M = truth.size();
