@@ -85,3 +85,20 @@ def test_no_cpu_fallback_without_gpu(golden_dir):
     spec = load_model_spec(os.path.join(golden_dir, "heston_small.json"))
     with pytest.raises(engine.EngineError):
         engine.Engine(spec)
+
+
+def test_header_is_plain_c(tmp_path):
+    # the drop-in boundary must be consumable from C (cgo / ctypes / JNI shims):
+    # compile a translation unit that uses every declared type with gcc -std=c11
+    import subprocess
+    src = tmp_path / "use_abi.c"
+    src.write_text('#include "lanetape_b200.h"\n'
+                   "int main(void) {\n"
+                   "  ltg_heston_model h = {0}; ltg_basket_model b = {0}; ltg_mc_config c = {0};\n"
+                   "  ltg_report r = {0}; ltg_timing t = {0}; ltg_shard s = {0};\n"
+                   "  (void)h; (void)b; (void)c; (void)r; (void)t; (void)s;\n"
+                   "  return ltg_abi_version() == LTG_ABI_VERSION ? 0 : 1;\n}\n")
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-fsyntax-only",
+                        "-I", os.path.join(ROOT, "include"), str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
