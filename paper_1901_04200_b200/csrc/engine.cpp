@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -90,7 +91,10 @@ struct Nccl {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
+    std::mutex mu;
+
     bool load(std::string& why) {
+        std::lock_guard<std::mutex> lock(mu);  // contexts may attach from several threads
         if (lib) return true;
         lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
         if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
