@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define LTG_ABI_VERSION 1
+#define LTG_ABI_VERSION 2
 
 #define LTG_OK 0
 #define LTG_EINVAL 1
@@ -147,6 +147,9 @@ typedef struct ltg_timing {
     uint32_t seg_steps;          /* checkpoint interval used (Heston), 0 if none */
     uint64_t ckpt_bytes;         /* HBM checkpoint / store table written by pass 1 */
     uint64_t z_bytes;            /* HBM draw store written by pass 1 (read by pass 2) */
+    uint32_t safe_rerun;         /* 1: a fast kernel flagged an out-of-range argument and
+                                    the call was redone with the exact slow paths */
+    uint32_t reserved;
 } ltg_timing;
 
 /* Path sharding plan: the path set is cut into fixed chunks whose size

@@ -941,7 +941,9 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
         const uint32_t nm = ctx->m;
         double* st = nullptr;
         for (ctx->safe = start_safe(ctx);; ctx->safe = 1) {
+            const uint32_t rerun = ctx->safe && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
+            ctx->timing.safe_rerun = rerun;
             upload_x(ctx, x, targets);
             clear_rare(ctx);
             if (tangent) {
@@ -1011,7 +1013,9 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
             ~Reset() { c->path_base = 0; }
         } reset{ctx};
         for (ctx->safe = start_safe(ctx);; ctx->safe = 1) {
+            const uint32_t rerun = ctx->safe && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
+            ctx->timing.safe_rerun = rerun;
             ctx->path_base = path0;
             upload_x(ctx, x, nullptr);
             clear_rare(ctx);
@@ -1050,7 +1054,9 @@ int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_con
         const uint32_t nm = ctx->m;
         double* st = nullptr;
         for (ctx->safe = start_safe(ctx);; ctx->safe = 1) {
+            const uint32_t rerun = ctx->safe && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
+            ctx->timing.safe_rerun = rerun;
             upload_x(ctx, x, nullptr);
             clear_rare(ctx);
             run_pass1(ctx, *cfg, plan, false, false);

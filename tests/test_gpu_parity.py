@@ -505,3 +505,26 @@ def test_cfg5_end_to_end_2p22(ref):
     orc = prog.gradient_of_G(c.x, t, c.paths, c.seed, workers=os.cpu_count())
     rep = Engine(c.spec).gradient_of_G(c.x, t, MCConfig(paths=c.paths, seed=c.seed))
     assert_report_close(rep, orc)
+
+
+def test_rare_flag_reruns_exactly(ref):
+    # v0 = 1e-300: the first step's sqrt(V) is outside the fast sqrt's exact
+    # range (V < 2^-970), which the fast step flags (heston.cu heston_step) —
+    # the call must be redone with the exact kernels and still match the
+    # reference; a sane call must not rerun
+    c = configs.cfg3()
+    eng = Engine(c.spec)
+    prog = ref.program(c.spec)
+    t = configs.load_targets(c)
+    cfg = MCConfig(paths=3000, seed=c.seed)
+    eng.gradient_of_G(c.x, t, cfg)
+    assert eng.timing()["safe_rerun"] == 0
+    x = list(c.x)
+    x[4] = 1e-300
+    orc = prog.gradient_of_G(x, t, 3000, c.seed, workers=8)
+    rep = eng.gradient_of_G(x, t, cfg)
+    assert eng.timing()["safe_rerun"] == 1
+    assert_report_close(rep, orc)
+    rep_t = eng.gradient_of_G(x, t, cfg, method="tangent")
+    assert eng.timing()["safe_rerun"] == 1
+    assert_report_close(rep_t, orc)
