@@ -42,17 +42,24 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi sampling of the SM clock and throttle reasons (B200_PROFILING.md).
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Started before the warm-up so that nvidia-smi's own start-up (NVML init)
+    is not inside the timed region; summary() keeps the samples whose
+    timestamps fall in the timed window (or the one nearest to it when the
+    window is shorter than the 200 ms sampling period)."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.lines = []
+        self.window = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
@@ -62,8 +69,11 @@ class Clocks:
             self.proc = None
         return self
 
-    def __exit__(self, *exc):
-        self.lines = []
+    def mark(self, t0: float, t1: float):
+        """the timed region, in time.time() seconds"""
+        self.window = (t0, t1)
+
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -72,23 +82,32 @@ class Clocks:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
             self.lines = [l for l in out.splitlines() if l.strip()]
+            self.proc = None
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        rows = []
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[2]), float(f[3]),
+                             {n for n, v in zip(names, f[6:10]) if v.lower() == "active"}))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+        if self.window and rows:
+            t0, t1 = self.window
+            inside = [r for r in rows if t0 <= r[0] <= t1]
+            if not inside:  # shorter than one sampling period: the nearest sample
+                inside = [min(rows, key=lambda r: min(abs(r[0] - t0), abs(r[0] - t1)))]
+            rows = inside
+        sm = [r[1] for r in rows]
+        reasons = set().union(*[r[3] for r in rows]) if rows else set()
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": rows[-1][2] if rows else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -210,6 +229,7 @@ def main():
     mc = MCConfig(paths=cfg.paths, seed=cfg.seed,
                   precision=FP32 if args.precision == "fp32" else FP64)
 
+    clk = Clocks(local).start()
     for _ in range(args.warmup):
         eng.gradient_of_G(cfg.x, targets, mc, method=args.method)
 
@@ -217,17 +237,19 @@ def main():
     if pg:
         pg.barrier()
     dev_ms, p1_ms, p2_ms, launches = [], [], [], 0
-    with Clocks(local) as clk:
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            # host buffers in, report out, synced
-            rep = eng.gradient_of_G(cfg.x, targets, mc, method=args.method)
-            tm = eng.timing()
-            dev_ms.append(tm["total_ms"])
-            p1_ms.append(tm["pass1_ms"])
-            p2_ms.append(tm["pass2_ms"])
-            launches += tm["launches"]
-        wall = time.perf_counter() - t0
+    e0 = time.time()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        # host buffers in, report out, synced
+        rep = eng.gradient_of_G(cfg.x, targets, mc, method=args.method)
+        tm = eng.timing()
+        dev_ms.append(tm["total_ms"])
+        p1_ms.append(tm["pass1_ms"])
+        p2_ms.append(tm["pass2_ms"])
+        launches += tm["launches"]
+    wall = time.perf_counter() - t0
+    clk.mark(e0, time.time())
+    clk.stop()
     clocks = clk.summary()
     dev_total = sum(dev_ms)
     if pg:
