@@ -60,6 +60,7 @@ class Clocks:
         self.window = None
 
     def start(self):
+        self.t_start = time.time()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
@@ -75,6 +76,9 @@ class Clocks:
 
     def stop(self):
         if self.proc:
+            # a short run still gets the first samples (nvidia-smi needs a few
+            # hundred ms to start): summary() then takes the nearest one
+            time.sleep(max(0.0, 0.8 - (time.time() - self.t_start)))
             self.proc.terminate()
             try:
                 out, _ = self.proc.communicate(timeout=5)
