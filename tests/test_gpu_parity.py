@@ -528,3 +528,23 @@ def test_rare_flag_reruns_exactly(ref):
     rep_t = eng.gradient_of_G(x, t, cfg, method="tangent")
     assert eng.timing()["safe_rerun"] == 1
     assert_report_close(rep_t, orc)
+
+
+@pytest.mark.parametrize("name,paths,seed,anti,fresh,method", [
+    ("cfg2", 3001, 42, True, False, "adjoint"),
+    ("cfg2", 2048, (1 << 40) + 7, False, True, "adjoint"),
+    ("cfg1", 5000, (1 << 63) + 11, True, False, "adjoint"),
+    ("cfg1", 4096, (1 << 35) + 3, False, True, "tangent"),
+    ("cfg3", 2500, (1 << 50) + 1, True, True, "adjoint"),
+    ("cfg3", 2500, (1 << 50) + 1, True, True, "tangent"),
+])
+def test_option_combinations_match_reference(ref, name, paths, seed, anti, fresh, method):
+    # MCConfig options crossed with 64-bit seeds (the Philox key's high word)
+    c = configs.ALL[name]()
+    eng = Engine(c.spec)
+    prog = ref.program(c.spec)
+    t = configs.load_targets(c) or _targets_from(prog, c.truth, paths, 4242)
+    orc = prog.gradient_of_G(c.x, t, paths, seed, antithetic=anti, fresh=fresh, workers=8)
+    rep = eng.gradient_of_G(c.x, t, MCConfig(paths=paths, seed=seed, antithetic=anti,
+                                             fresh_step2_paths=fresh), method=method)
+    assert_report_close(rep, orc)
