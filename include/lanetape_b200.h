@@ -168,6 +168,17 @@ int ltg_abi_version(void);
 
 int ltg_create_heston(const ltg_heston_model* model, int device, ltg_ctx** out);
 int ltg_create_basket(const ltg_basket_model* model, int device, ltg_ctx** out);
+/* Single-process multi-GPU context (the reference's host is one process):
+ * one member context per listed device, NCCL communicators from
+ * ncclCommInitAll, member i = rank i. Every compute call then runs on all
+ * devices concurrently (one host thread each), sharded and reduced exactly as
+ * ltg_attach_nccl's one-process-per-GPU mode — the same bits for any device
+ * count. Single-device diagnostics (fill_normals, inverse_normal,
+ * path_payoffs, chunk_sums) run on the first device. */
+int ltg_create_heston_devices(const ltg_heston_model* model, const int* devices, int n,
+                              ltg_ctx** out);
+int ltg_create_basket_devices(const ltg_basket_model* model, const int* devices, int n,
+                              ltg_ctx** out);
 void ltg_destroy(ltg_ctx* ctx);
 const char* ltg_last_error(const ltg_ctx* ctx);
 

@@ -110,10 +110,16 @@ inline ltg_mc_config to_c(const MCConfig& c) {
 }
 }  // namespace detail
 
-// A Heston-SLV program bound to one GPU.
+// A Heston-SLV program bound to one GPU, or (the devices constructor) to
+// several GPUs of this process: every call then shards the paths over them
+// (ltg_create_heston_devices) with the same results.
 class Engine {
 public:
-    explicit Engine(const ModelSpec& s, int device = 0) {
+    explicit Engine(const ModelSpec& s, int device = 0) : Engine(s, std::vector<int>{device}, false) {}
+    Engine(const ModelSpec& s, const std::vector<int>& devices) : Engine(s, devices, true) {}
+
+private:
+    Engine(const ModelSpec& s, const std::vector<int>& devices, bool group) {
         std::vector<int32_t> kind;
         std::vector<double> strike;
         std::vector<uint32_t> mat;
@@ -141,8 +147,13 @@ public:
         m.n_instruments = static_cast<uint32_t>(kind.size());
         m.steps = static_cast<uint32_t>(s.mc.steps);
         m.dt = s.mc.dt;
-        detail::check(ltg_create_heston(&m, device, &ctx_), ltg_last_error(nullptr));
+        const int rc = group ? ltg_create_heston_devices(&m, devices.data(),
+                                                         static_cast<int>(devices.size()), &ctx_)
+                             : ltg_create_heston(&m, devices.at(0), &ctx_);
+        detail::check(rc, ltg_last_error(nullptr));
     }
+
+public:
     explicit Engine(const ltg_basket_model& m, int device = 0) {
         detail::check(ltg_create_basket(&m, device, &ctx_), ltg_last_error(nullptr));
     }

@@ -26,6 +26,7 @@
 #include <memory>
 #include <mutex>
 #include <numeric>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -84,6 +85,7 @@ struct Nccl {
     void* lib = nullptr;
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
@@ -104,13 +106,14 @@ struct Nccl {
         }
         GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
         CommInitRank = reinterpret_cast<decltype(CommInitRank)>(dlsym(lib, "ncclCommInitRank"));
+        CommInitAll = reinterpret_cast<decltype(CommInitAll)>(dlsym(lib, "ncclCommInitAll"));
         AllGather = reinterpret_cast<decltype(AllGather)>(dlsym(lib, "ncclAllGather"));
         AllReduce = reinterpret_cast<decltype(AllReduce)>(dlsym(lib, "ncclAllReduce"));
         CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(lib, "ncclCommDestroy"));
         GetErrorString =
             reinterpret_cast<decltype(GetErrorString)>(dlsym(lib, "ncclGetErrorString"));
-        if (!GetUniqueId || !CommInitRank || !AllGather || !AllReduce || !CommDestroy ||
-            !GetErrorString) {
+        if (!GetUniqueId || !CommInitRank || !CommInitAll || !AllGather || !AllReduce ||
+            !CommDestroy || !GetErrorString) {
             why = "libnccl.so.2 lacks required symbols";
             return false;
         }
@@ -149,6 +152,10 @@ uint64_t chunks_per_rank(const ltg_shard& s, int world) {
 }  // namespace
 
 struct ltg_ctx {
+    // single-process multi-GPU context (ltg_create_*_devices): one member
+    // context per device, member i = NCCL rank i; the group itself has no
+    // device state and runs every call on all members concurrently
+    std::vector<std::unique_ptr<ltg_ctx>> members;
     int kind = 0;  // 0 Heston SLV, 1 basket
     uint64_t path_base = 0;  // global index of path 0 of a call (ltg_chunk_sums; else 0)
     bool ready = false;  // device state initialised
@@ -231,6 +238,51 @@ int guarded(ltg_ctx* ctx, Fn&& fn) {
 
 void require(bool ok, const std::string& msg) {
     if (!ok) throw Failure(LTG_EINVAL, msg);
+}
+
+bool is_group(const ltg_ctx* c) { return c && !c->members.empty(); }
+
+// Run fn(member, index) on every member of a multi-GPU context, one host
+// thread per device (their NCCL collectives meet), and report the first
+// failure. Validation failures happen identically on every member before any
+// collective, so a bad argument cannot leave some members waiting.
+template <typename Fn>
+int group_run(ltg_ctx* g, Fn&& fn) {
+    const size_t n = g->members.size();
+    std::vector<int> rc(n, LTG_OK);
+    std::vector<std::thread> threads;
+    for (size_t i = 1; i < n; ++i)
+        threads.emplace_back([&, i] { rc[i] = fn(g->members[i].get(), i); });
+    rc[0] = fn(g->members[0].get(), size_t(0));
+    for (auto& t : threads) t.join();
+    for (size_t i = 0; i < n; ++i)
+        if (rc[i] != LTG_OK) {
+            g->err = g->members[i]->err;
+            return rc[i];
+        }
+    g->timing = g->members[0]->timing;  // with the slowest member's total
+    for (const auto& m : g->members)
+        g->timing.total_ms = std::max(g->timing.total_ms, m->timing.total_ms);
+    return LTG_OK;
+}
+
+// A single-device diagnostic (draws, per-path outputs, chunk sums) on member
+// 0, its communicator detached for the call.
+template <typename Fn>
+int group_solo(ltg_ctx* g, Fn&& fn) {
+    ltg_ctx* m = g->members[0].get();
+    const ncclComm_t comm = m->comm;
+    const int rank = m->rank, world = m->world;
+    m->comm = nullptr;
+    m->rank = 0;
+    m->world = 1;
+    const int rc = fn(m);
+    m->comm = comm;
+    m->rank = rank;
+    m->world = world;
+    if (rc != LTG_OK) g->err = m->err;
+    g->timing = m->timing;
+    return rc;
 }
 
 template <typename T>
@@ -748,6 +800,58 @@ void upload_x(ltg_ctx* c, const double* x, const double* targets) {
 
 }  // namespace
 
+namespace {
+
+// ltg_create_*_devices: one member context per device plus ncclCommInitAll
+template <typename Create>
+int create_group(const int* devices, int n, ltg_ctx** out, Create create) {
+    if (!out || !devices || n < 1) {
+        g_create_error = "create_devices: need an output pointer and >= 1 device";
+        return LTG_EINVAL;
+    }
+    *out = nullptr;
+    auto g = std::make_unique<ltg_ctx>();
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < i; ++j)
+            if (devices[j] == devices[i]) {
+                g_create_error = "create_devices: a device may appear once";
+                return LTG_EINVAL;
+            }
+        ltg_ctx* m = nullptr;
+        const int rc = create(devices[i], &m);
+        if (rc != LTG_OK) return rc;  // g_create_error set by the member's create
+        g->members.emplace_back(m);
+    }
+    std::string why;
+    if (!nccl().load(why)) {
+        g_create_error = why;
+        return LTG_ECUDA;
+    }
+    std::vector<ncclComm_t> comms(n);
+    const ncclResult_t r = nccl().CommInitAll(comms.data(), n, devices);
+    if (r != ncclSuccess) {
+        g_create_error = std::string("ncclCommInitAll: ") + nccl().GetErrorString(r);
+        return LTG_ECUDA;
+    }
+    for (int i = 0; i < n; ++i) {
+        g->members[i]->comm = comms[i];
+        g->members[i]->rank = i;
+        g->members[i]->world = n;
+    }
+    const ltg_ctx& m0 = *g->members[0];
+    g->kind = m0.kind;
+    g->M = m0.M;
+    g->m = m0.m;
+    g->N = m0.N;
+    g->x0 = m0.x0;
+    g->h_rc = m0.h_rc;
+    g->device = m0.device;
+    *out = g.release();
+    return LTG_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 int ltg_abi_version(void) { return LTG_ABI_VERSION; }
@@ -891,6 +995,21 @@ int ltg_create_basket(const ltg_basket_model* mdl, int device, ltg_ctx** out) {
     return LTG_OK;
 }
 
+
+int ltg_create_heston_devices(const ltg_heston_model* model, const int* devices, int n,
+                              ltg_ctx** out) {
+    return create_group(devices, n, out, [&](int dev, ltg_ctx** m) {
+        return ltg_create_heston(model, dev, m);
+    });
+}
+
+int ltg_create_basket_devices(const ltg_basket_model* model, const int* devices, int n,
+                              ltg_ctx** out) {
+    return create_group(devices, n, out, [&](int dev, ltg_ctx** m) {
+        return ltg_create_basket(model, dev, m);
+    });
+}
+
 void ltg_destroy(ltg_ctx* ctx) { delete ctx; }
 
 const char* ltg_last_error(const ltg_ctx* ctx) {
@@ -922,6 +1041,21 @@ namespace {
 int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets, size_t m,
                   const ltg_mc_config* cfg, ltg_report* report, bool tangent) {
     if (!ctx) return LTG_EINVAL;
+    if (is_group(ctx)) {
+        const ltg_report proto = report ? *report : ltg_report{};
+        return group_run(ctx, [&](ltg_ctx* mb, size_t i) {
+            if (i == 0) return gradient_impl(mb, x, M, targets, m, cfg, report, tangent);
+            // the other ranks' identical reports land in scratch (same nullness,
+            // so every member validates alike)
+            std::vector<double> means(ctx->m), lambda(ctx->m), grad(ctx->M), se(ctx->m);
+            ltg_report r = proto;
+            r.means = proto.means ? means.data() : nullptr;
+            r.lambda = proto.lambda ? lambda.data() : nullptr;
+            r.grad = proto.grad ? grad.data() : nullptr;
+            r.std_errors = proto.std_errors ? se.data() : nullptr;
+            return gradient_impl(mb, x, M, targets, m, cfg, report ? &r : nullptr, tangent);
+        });
+    }
     return guarded(ctx, [&] {
         validate_cfg(ctx, cfg, M);
         require(x && targets && report && report->means && report->lambda && report->grad,
@@ -1001,6 +1135,11 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
                    uint64_t seed, int antithetic, uint64_t path0, uint64_t npaths,
                    double* sums, double* sumsq, double* adjoint) {
     if (!ctx) return LTG_EINVAL;
+    if (is_group(ctx))
+        return group_solo(ctx, [&](ltg_ctx* mb) {
+            return ltg_chunk_sums(mb, x, M, lambda, m, seed, antithetic, path0, npaths, sums,
+                                  sumsq, adjoint);
+        });
     return guarded(ctx, [&] {
         require(x && lambda && sums && sumsq && adjoint, "null buffer");
         require(M == ctx->M && m == ctx->m, "chunk_sums: size mismatch");
@@ -1046,6 +1185,13 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
 int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg,
                        double* means, double* std_errors) {
     if (!ctx) return LTG_EINVAL;
+    if (is_group(ctx))
+        return group_run(ctx, [&](ltg_ctx* mb, size_t i) {
+            if (i == 0) return ltg_estimate_means(mb, x, M, cfg, means, std_errors);
+            std::vector<double> mv(ctx->m), sv(ctx->m);
+            return ltg_estimate_means(mb, x, M, cfg, means ? mv.data() : nullptr,
+                                      std_errors ? sv.data() : nullptr);
+        });
     return guarded(ctx, [&] {
         validate_cfg(ctx, cfg, M);
         require(x && means, "null buffer");
@@ -1081,6 +1227,13 @@ int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_con
 int ltg_finite_diff_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
                                   size_t m, const ltg_mc_config* cfg, double h, double* grad) {
     if (!ctx) return LTG_EINVAL;
+    if (is_group(ctx))
+        return group_run(ctx, [&](ltg_ctx* mb, size_t i) {
+            if (i == 0) return ltg_finite_diff_gradient_of_G(mb, x, M, targets, m, cfg, h, grad);
+            std::vector<double> g(ctx->M);
+            return ltg_finite_diff_gradient_of_G(mb, x, M, targets, m, cfg, h,
+                                                 grad ? g.data() : nullptr);
+        });
     if (!(h > 0.0)) {
         ctx->err = "finite_diff_gradient_of_G: h must be > 0";
         return LTG_EINVAL;
@@ -1120,6 +1273,10 @@ int ltg_finite_diff_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const
 int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, uint64_t path0,
                      uint64_t npaths, double* out) {
     if (!ctx) return LTG_EINVAL;
+    if (is_group(ctx))
+        return group_solo(ctx, [&](ltg_ctx* mb) {
+            return ltg_fill_normals(mb, seed, dim, antithetic, path0, npaths, out);
+        });
     return guarded(ctx, [&] {
         require(out != nullptr, "null buffer");
         require(dim > 0 && dim < (size_t(1) << 30), "dimension out of range");
@@ -1139,6 +1296,8 @@ int ltg_fill_normals(ltg_ctx* ctx, uint64_t seed, size_t dim, int antithetic, ui
 
 int ltg_inverse_normal(ltg_ctx* ctx, const double* p, size_t n, double* z) {
     if (!ctx) return LTG_EINVAL;
+    if (is_group(ctx))
+        return group_solo(ctx, [&](ltg_ctx* mb) { return ltg_inverse_normal(mb, p, n, z); });
     return guarded(ctx, [&] {
         require(p && z, "null buffer");
         if (n == 0) return;
@@ -1158,6 +1317,10 @@ int ltg_inverse_normal(ltg_ctx* ctx, const double* p, size_t n, double* z) {
 int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int antithetic,
                      uint64_t path0, uint64_t npaths, double* y) {
     if (!ctx) return LTG_EINVAL;
+    if (is_group(ctx))
+        return group_solo(ctx, [&](ltg_ctx* mb) {
+            return ltg_path_payoffs(mb, x, M, seed, antithetic, path0, npaths, y);
+        });
     return guarded(ctx, [&] {
         require(x && y && M == ctx->M, "path_payoffs: size mismatch");
         check_params(ctx, x);
@@ -1224,6 +1387,10 @@ int ltg_nccl_unique_id(unsigned char id[128]) {
 
 int ltg_attach_nccl(ltg_ctx* ctx, const unsigned char id[128], int rank, int world) {
     if (!ctx) return LTG_EINVAL;
+    if (is_group(ctx)) {
+        ctx->err = "attach_nccl: a multi-device context has its communicators already";
+        return LTG_EINVAL;
+    }
     return guarded(ctx, [&] {
         require(id != nullptr && world >= 1 && rank >= 0 && rank < world, "bad rank/world");
         std::string why;

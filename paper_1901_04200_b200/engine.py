@@ -47,6 +47,9 @@ def load_library(path: str = LIB_PATH):
     L.ltg_abi_version.restype = C.c_int
     L.ltg_create_heston.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
     L.ltg_create_basket.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+    L.ltg_create_heston_devices.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.c_int,
+                                            C.POINTER(C.c_void_p)]
+    L.ltg_create_basket_devices.argtypes = L.ltg_create_heston_devices.argtypes
     L.ltg_destroy.argtypes = [C.c_void_p]
     L.ltg_last_error.argtypes = [C.c_void_p]
     L.ltg_last_error.restype = C.c_char_p
@@ -139,13 +142,22 @@ class Engine:
     """A model bound to one GPU: the GPU counterpart of a recorded program
     (record_heston_program(ModelSpec) for Heston-SLV; the config-4 basket)."""
 
-    def __init__(self, spec, device: int = 0):
+    def __init__(self, spec, device: int = 0, devices: Optional[Sequence[int]] = None):
+        """devices: a single-process multi-GPU context over these devices
+        (ltg_create_*_devices); otherwise one context on `device`."""
         self.lib = load_library()
         self.spec = spec
         self._mm = MarshalledModel(spec)
         h = C.c_void_p()
-        fn = self.lib.ltg_create_heston if self._mm.kind == 0 else self.lib.ltg_create_basket
-        rc = fn(C.cast(self._mm.ptr, C.c_void_p), device, C.byref(h))
+        model = C.cast(self._mm.ptr, C.c_void_p)
+        if devices is not None:
+            devs = (C.c_int * len(devices))(*devices)
+            fn = (self.lib.ltg_create_heston_devices if self._mm.kind == 0
+                  else self.lib.ltg_create_basket_devices)
+            rc = fn(model, devs, len(devices), C.byref(h))
+        else:
+            fn = self.lib.ltg_create_heston if self._mm.kind == 0 else self.lib.ltg_create_basket
+            rc = fn(model, device, C.byref(h))
         if rc:
             msg = self.lib.ltg_last_error(None).decode()
             raise (ValueError if rc == LTG_EINVAL else EngineError)(msg)

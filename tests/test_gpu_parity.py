@@ -548,3 +548,31 @@ def test_option_combinations_match_reference(ref, name, paths, seed, anti, fresh
     rep = eng.gradient_of_G(c.x, t, MCConfig(paths=paths, seed=seed, antithetic=anti,
                                              fresh_step2_paths=fresh), method=method)
     assert_report_close(rep, orc)
+
+
+def test_single_process_device_group():
+    # ltg_create_*_devices: a one-device group (all this environment has) runs
+    # every call through the group path (member threads, ncclCommInitAll
+    # communicators, the in-place all-gather) and must equal the plain context
+    c = configs.cfg3()
+    t = configs.load_targets(c)
+    cfg = MCConfig(paths=4099, seed=c.seed)
+    plain = Engine(c.spec)
+    grp = Engine(c.spec, devices=[0])
+    assert grp.M == plain.M and grp.m == plain.m and grp.rng_exact
+    assert grp.gradient_of_G(c.x, t, cfg).to_json() == plain.gradient_of_G(c.x, t, cfg).to_json()
+    assert grp.gradient_of_G(c.x, t, cfg, method="tangent").to_json() == \
+        plain.gradient_of_G(c.x, t, cfg, method="tangent").to_json()
+    assert grp.estimate_means(c.x, cfg).means == plain.estimate_means(c.x, cfg).means
+    assert np.array_equal(grp.fill_normals(7, 8, False, 3, 64), plain.fill_normals(7, 8, False, 3, 64))
+    assert grp.timing()["total_ms"] > 0
+    from paper_1901_04200_b200.engine import nccl_unique_id
+    with pytest.raises(ValueError):
+        grp.attach_nccl(nccl_unique_id(), 0, 1)
+    b = configs.cfg4()
+    bg = Engine(b.spec, devices=[0])
+    cfg4 = MCConfig(paths=2048, seed=b.seed)
+    assert bg.gradient_of_G(b.x, b.targets, cfg4).to_json() == \
+        Engine(b.spec).gradient_of_G(b.x, b.targets, cfg4).to_json()
+    with pytest.raises(ValueError):
+        Engine(c.spec, devices=[0, 0])
