@@ -60,6 +60,9 @@ class Clocks:
         self.window = None
 
     def start(self):
+        """start sampling and wait (<= 3 s) for the first sample, so that the
+        sampler's own start-up (NVML init) is over before anything is timed"""
+        import threading
         self.t_start = time.time()
         try:
             self.proc = subprocess.Popen(
@@ -68,6 +71,19 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return self
+        first = threading.Event()
+
+        def reader():
+            for line in self.proc.stdout:
+                if line.strip():
+                    self.lines.append(line.strip())
+                    first.set()
+            first.set()
+
+        self.reader = threading.Thread(target=reader, daemon=True)
+        self.reader.start()
+        first.wait(3.0)
         return self
 
     def mark(self, t0: float, t1: float):
@@ -76,16 +92,13 @@ class Clocks:
 
     def stop(self):
         if self.proc:
-            # a short run still gets the first samples (nvidia-smi needs a few
-            # hundred ms to start): summary() then takes the nearest one
-            time.sleep(max(0.0, 0.8 - (time.time() - self.t_start)))
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
+                self.proc.wait()
+            self.reader.join(timeout=5)
             self.proc = None
 
     def summary(self):
