@@ -350,7 +350,7 @@ def main():
         if trf is not None and args.method == "adjoint":
             # ncu bytes/path without the draw store (checkpoint table), plus
             # the draw store this call wrote (pass 1) and read back (pass 2):
-            # pass 2 with draws measures 1,527 + 756*16 B/path (r1_v9_cfg3_full)
+            # pass 2 with draws measures 1,527 + 756*16 B/path (profiles/r1_v12_cfg3_full.txt)
             roof["traffic"] = trf * paths_rank + tm["z_bytes"]
         M, m = len(cfg.x), cfg.m
         line = {

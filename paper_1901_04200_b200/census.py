@@ -30,9 +30,9 @@ PASS2_FP64 = {"cfg3_heston:fp64": 143004.0, "cfg1_gbm:fp64": 2960.0,
 PASS1_FP32 = {"cfg3_heston:fp32": 45249.3}
 PASS2_FP32 = {"cfg3_heston:fp32": 67958.8}
 # per-path DRAM bytes (ncu dram__bytes_read+write / paths), latest capture without the
-# draw store (profiles/r1_v9_cfg3_noz_full.txt: the regime of cfg5 on one GPU)
-PASS1_DRAM = {"cfg3_heston:fp64": 1457.1}
-PASS2_DRAM = {"cfg3_heston:fp64": 1526.6}
+# draw store (profiles/r1_v12_cfg3_noz_full.txt: the regime of cfg5 on one GPU)
+PASS1_DRAM = {"cfg3_heston:fp64": 1455.8}
+PASS2_DRAM = {"cfg3_heston:fp64": 1526.4}
 
 
 def _key(name: str, precision: str):
