@@ -576,3 +576,21 @@ def test_single_process_device_group():
         Engine(b.spec).gradient_of_G(b.x, b.targets, cfg4).to_json()
     with pytest.raises(ValueError):
         Engine(c.spec, devices=[0, 0])
+
+
+@pytest.mark.parametrize("anti,fresh", [(True, False), (False, True), (True, True)])
+def test_fp32_option_combinations(ref, anti, fresh):
+    # the fp32 variant under antithetic draws / fresh step-2 paths, at the
+    # fp32 tolerances of DESIGN.md §6 against the fp64 reference
+    from paper_1901_04200_b200.model import FP32
+    c = configs.cfg3()
+    t = configs.load_targets(c)
+    prog = ref.program(c.spec)
+    paths = 1 << 13
+    orc = prog.gradient_of_G(c.x, t, paths, c.seed, antithetic=anti, fresh=fresh, workers=8)
+    rep = Engine(c.spec).gradient_of_G(c.x, t, MCConfig(paths=paths, seed=c.seed, antithetic=anti,
+                                                        fresh_step2_paths=fresh, precision=FP32))
+    tol = FP32_TOL["cfg3"]
+    assert rel_err(rep.means, orc["means"], 1e-6) <= tol["means"]
+    assert rel_err([rep.G], [orc["G"]]) <= tol["G"]
+    assert rel_err(rep.grad, orc["grad"], 1e-3) <= tol["grad"]
