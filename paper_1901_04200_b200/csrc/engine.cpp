@@ -26,6 +26,7 @@
 #include <memory>
 #include <mutex>
 #include <numeric>
+#include <condition_variable>
 #include <thread>
 #include <stdexcept>
 #include <string>
@@ -151,11 +152,39 @@ uint64_t chunks_per_rank(const ltg_shard& s, int world) {
 
 }  // namespace
 
+// Test-only in-process collective for member contexts that share one GPU
+// (LTG_LOOPBACK=1 with ltg_create_*_devices): the exchanges NCCL performs,
+// done with device-to-device copies between the members' tables and a host
+// barrier, so the multi-rank code paths (shard plans, per-rank rows, the
+// all-gather layout, the rare-flag reduction) run for real on one GPU.
+struct Loopback {
+    explicit Loopback(int w) : world(w), tables(w, nullptr), flags(w, 0) {}
+    int world;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t generation = 0;
+    std::vector<double*> tables;
+    std::vector<uint32_t> flags;
+    void barrier() {
+        std::unique_lock<std::mutex> lock(mu);
+        const uint64_t gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lock, [&] { return generation != gen; });
+        }
+    }
+};
+
 struct ltg_ctx {
     // single-process multi-GPU context (ltg_create_*_devices): one member
     // context per device, member i = NCCL rank i; the group itself has no
     // device state and runs every call on all members concurrently
     std::vector<std::unique_ptr<ltg_ctx>> members;
+    std::shared_ptr<Loopback> loop;  // test-only collective instead of NCCL (see Loopback)
     int kind = 0;  // 0 Heston SLV, 1 basket
     uint64_t path_base = 0;  // global index of path 0 of a call (ltg_chunk_sums; else 0)
     bool ready = false;  // device state initialised
@@ -272,12 +301,15 @@ template <typename Fn>
 int group_solo(ltg_ctx* g, Fn&& fn) {
     ltg_ctx* m = g->members[0].get();
     const ncclComm_t comm = m->comm;
+    const std::shared_ptr<Loopback> loop = m->loop;
     const int rank = m->rank, world = m->world;
     m->comm = nullptr;
+    m->loop = nullptr;
     m->rank = 0;
     m->world = 1;
     const int rc = fn(m);
     m->comm = comm;
+    m->loop = loop;
     m->rank = rank;
     m->world = world;
     if (rc != LTG_OK) g->err = m->err;
@@ -342,6 +374,21 @@ size_t floor_index(const std::vector<double>& nodes, double x) {
 }
 
 void all_gather_rows(ltg_ctx* c, double* table, uint64_t per_rank, uint32_t width) {
+    if (c->loop) {
+        Loopback& L = *c->loop;
+        const size_t count = size_t(per_rank) * width;
+        cuda_check(cudaStreamSynchronize(c->stream), "synchronize");  // own rows written
+        L.tables[c->rank] = table;
+        L.barrier();  // every member's rows are written
+        for (int r = 0; r < L.world; ++r)
+            if (r != c->rank)
+                cuda_check(cudaMemcpyAsync(table + size_t(r) * count, L.tables[r] + size_t(r) * count,
+                                           count * 8, cudaMemcpyDeviceToDevice, c->stream),
+                           "loopback all-gather");
+        cuda_check(cudaStreamSynchronize(c->stream), "synchronize");
+        L.barrier();  // no member reuses its table before every copy is done
+        return;
+    }
     if (!c->comm) return;  // (an attached single-rank comm still runs the collective)
     const size_t count = size_t(per_rank) * width;
     const ncclResult_t r = nccl().AllGather(table + size_t(c->rank) * count, table, count,
@@ -769,6 +816,20 @@ void clear_rare(ltg_ctx* c) {
 
 bool take_rare(ltg_ctx* c, double* host_slot) {
     uint32_t* d = c->d_counter.as<uint32_t>() + kRareSlot;
+    if (c->loop) {
+        Loopback& L = *c->loop;
+        uint32_t v = 0;
+        cuda_check(cudaMemcpyAsync(host_slot, d, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                   c->stream),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(c->stream), "synchronize");
+        std::memcpy(&v, host_slot, sizeof v);
+        L.flags[c->rank] = v;
+        L.barrier();
+        for (uint32_t f : L.flags) v = std::max(v, f);
+        L.barrier();
+        return v != 0;
+    }
     if (c->comm) {
         const ncclResult_t r = nccl().AllReduce(d, d, 1, ncclUint32, ncclMax, c->comm, c->stream);
         if (r != ncclSuccess)
@@ -810,9 +871,11 @@ int create_group(const int* devices, int n, ltg_ctx** out, Create create) {
         return LTG_EINVAL;
     }
     *out = nullptr;
+    const char* lb = std::getenv("LTG_LOOPBACK");
+    const bool loopback = lb && lb[0] == '1';  // tests: members may share a device
     auto g = std::make_unique<ltg_ctx>();
     for (int i = 0; i < n; ++i) {
-        for (int j = 0; j < i; ++j)
+        for (int j = 0; j < i && !loopback; ++j)
             if (devices[j] == devices[i]) {
                 g_create_error = "create_devices: a device may appear once";
                 return LTG_EINVAL;
@@ -822,6 +885,14 @@ int create_group(const int* devices, int n, ltg_ctx** out, Create create) {
         if (rc != LTG_OK) return rc;  // g_create_error set by the member's create
         g->members.emplace_back(m);
     }
+    if (loopback) {
+        auto L = std::make_shared<Loopback>(n);
+        for (int i = 0; i < n; ++i) {
+            g->members[i]->loop = L;
+            g->members[i]->rank = i;
+            g->members[i]->world = n;
+        }
+    } else {
     std::string why;
     if (!nccl().load(why)) {
         g_create_error = why;
@@ -837,6 +908,7 @@ int create_group(const int* devices, int n, ltg_ctx** out, Create create) {
         g->members[i]->comm = comms[i];
         g->members[i]->rank = i;
         g->members[i]->world = n;
+    }
     }
     const ltg_ctx& m0 = *g->members[0];
     g->kind = m0.kind;

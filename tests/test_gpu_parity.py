@@ -594,3 +594,45 @@ def test_fp32_option_combinations(ref, anti, fresh):
     assert rel_err(rep.means, orc["means"], 1e-6) <= tol["means"]
     assert rel_err([rep.G], [orc["G"]]) <= tol["G"]
     assert rel_err(rep.grad, orc["grad"], 1e-3) <= tol["grad"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_paths_on_one_gpu(world):
+    # LTG_LOOPBACK=1: `world` member contexts share the GPU and exchange their
+    # chunk rows with device copies where NCCL would all-gather, so every
+    # rank-dependent piece of the engine (shard plans, per-rank rows and
+    # checkpoint tables, the all-gather layout, the rare-flag reduction) runs
+    # for real; the reports must equal the one-context engine's bit for bit
+    import os
+    c = configs.cfg3()
+    t = configs.load_targets(c)
+    plain = Engine(c.spec)
+    os.environ["LTG_LOOPBACK"] = "1"
+    try:
+        grp = Engine(c.spec, devices=[0] * world)
+    finally:
+        os.environ.pop("LTG_LOOPBACK")
+    for cfg in (MCConfig(paths=50000 + 17, seed=c.seed),
+                MCConfig(paths=9001, seed=7, antithetic=True),
+                MCConfig(paths=4099, seed=c.seed, fresh_step2_paths=True)):
+        assert grp.gradient_of_G(c.x, t, cfg).to_json() == plain.gradient_of_G(c.x, t, cfg).to_json()
+        assert grp.gradient_of_G(c.x, t, cfg, method="tangent").to_json() == \
+            plain.gradient_of_G(c.x, t, cfg, method="tangent").to_json()
+        a, b = grp.estimate_means(c.x, cfg), plain.estimate_means(c.x, cfg)
+        assert a.means == b.means and a.std_errors == b.std_errors
+    # the rare-flag rerun agreed across ranks
+    x = list(c.x)
+    x[4] = 1e-300
+    cfg = MCConfig(paths=3000, seed=c.seed)
+    assert grp.gradient_of_G(x, t, cfg).to_json() == plain.gradient_of_G(x, t, cfg).to_json()
+    assert grp.timing()["safe_rerun"] == 1
+    # the basket (store-mode pass 2) across ranks
+    b4 = configs.cfg4()
+    os.environ["LTG_LOOPBACK"] = "1"
+    try:
+        bg = Engine(b4.spec, devices=[0] * world)
+    finally:
+        os.environ.pop("LTG_LOOPBACK")
+    cfg4 = MCConfig(paths=3001, seed=b4.seed)
+    assert bg.gradient_of_G(b4.x, b4.targets, cfg4).to_json() == \
+        Engine(b4.spec).gradient_of_G(b4.x, b4.targets, cfg4).to_json()
