@@ -235,6 +235,11 @@ int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int
 
 int ltg_last_timing(const ltg_ctx* ctx, ltg_timing* out);
 
+/* Cap (bytes, per GPU) of the HBM the context may hold for its checkpoint
+ * table and draw store; 0 (the default) uses the free device memory minus a
+ * 2 GiB reserve. Results do not depend on it, only the speed of pass 2. */
+int ltg_set_hbm_budget(ltg_ctx* ctx, uint64_t bytes);
+
 /* 1 when the GPU inverse-normal uses a log() validated bit-for-bit against
  * this host's libm (the reference's random stream is reproduced exactly);
  * 0 when that check failed and the GPU fell back to CUDA's log(). */

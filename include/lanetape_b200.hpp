@@ -216,6 +216,9 @@ public:
         return g;
     }
 
+    // HBM cap for the checkpoint table + draw store (0: the free memory)
+    void set_hbm_budget(std::uint64_t bytes) { detail::check(ltg_set_hbm_budget(ctx_, bytes), ""); }
+
     // Multi-GPU: rank r of `world` processes (one GPU each) sharing `id`
     // (from nccl_unique_id() on rank 0, broadcast by the caller).
     void attach_nccl(const unsigned char id[128], int rank, int world) {

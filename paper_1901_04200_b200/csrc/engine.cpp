@@ -185,6 +185,7 @@ struct ltg_ctx {
     // device state and runs every call on all members concurrently
     std::vector<std::unique_ptr<ltg_ctx>> members;
     std::shared_ptr<Loopback> loop;  // test-only collective instead of NCCL (see Loopback)
+    uint64_t hbm_budget = 0;         // ltg_set_hbm_budget: cap of checkpoints + draws (0: free HBM)
     int kind = 0;  // 0 Heston SLV, 1 basket
     uint64_t path_base = 0;  // global index of path 0 of a call (ltg_chunk_sums; else 0)
     bool ready = false;  // device state initialised
@@ -574,6 +575,7 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         // with other work); the default takes what is free
         if (const char* cap = std::getenv("LTG_HBM_BUDGET_GB"))
             avail = std::min<size_t>(avail, size_t(std::strtod(cap, nullptr) * double(1ull << 30)));
+        if (c->hbm_budget) avail = std::min<size_t>(avail, c->hbm_budget);
         const size_t elem = c->fp32 ? 8 : 16;
         const uint64_t nloc = w.n_chunks;
         const size_t z_chunk = size_t(c->steps) * plan.chunk_paths * elem;
@@ -688,6 +690,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
             if (budget < per_chunk * 64 && free_b > (size_t(2) << 30))
                 budget = std::max(budget, std::min(free_b - (size_t(2) << 30),
                                                    per_chunk * w.n_chunks));
+            if (c->hbm_budget) budget = std::min<size_t>(budget, c->hbm_budget);  // >= 1 chunk below
             uint64_t wave = std::max<uint64_t>(1, budget / per_chunk);
             wave = std::min<uint64_t>(wave, w.n_chunks);
             c->d_ckpt.ensure(wave * per_chunk);
@@ -1432,6 +1435,13 @@ int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int
                    "D2H");
         cuda_check(cudaStreamSynchronize(ctx->stream), "path payoffs");
     });
+}
+
+int ltg_set_hbm_budget(ltg_ctx* ctx, uint64_t bytes) {
+    if (!ctx) return LTG_EINVAL;
+    ctx->hbm_budget = bytes;
+    for (auto& m : ctx->members) m->hbm_budget = bytes;
+    return LTG_OK;
 }
 
 int ltg_last_timing(const ltg_ctx* ctx, ltg_timing* out) {

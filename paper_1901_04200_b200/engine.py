@@ -69,6 +69,7 @@ def load_library(path: str = LIB_PATH):
     L.ltg_chunk_sums.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, C.c_size_t, C.c_uint64,
                                  C.c_int, C.c_uint64, C.c_uint64, _dp, _dp, _dp]
     L.ltg_last_timing.argtypes = [C.c_void_p, C.POINTER(TimingC)]
+    L.ltg_set_hbm_budget.argtypes = [C.c_void_p, C.c_uint64]
     L.ltg_path_payoffs.argtypes = [C.c_void_p, _dp, C.c_size_t, C.c_uint64, C.c_int, C.c_uint64,
                                    C.c_uint64, _dp]
     L.ltg_rng_exact.argtypes = [C.c_void_p]
@@ -277,6 +278,12 @@ class Engine:
         if rc:
             self._raise(rc)
         return y
+
+    def set_hbm_budget(self, nbytes: int) -> None:
+        """Cap the HBM held for checkpoints + draw store (0: free memory)."""
+        rc = self.lib.ltg_set_hbm_budget(self.h, int(nbytes))
+        if rc:
+            self._raise(rc)
 
     def timing(self) -> dict:
         t = TimingC()

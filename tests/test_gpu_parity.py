@@ -297,6 +297,24 @@ def test_memory_plans_bitwise_identical(env):
     assert rep.to_json() == base.to_json()
 
 
+def test_hbm_budget_api():
+    # ltg_set_hbm_budget: a tiny budget forces the no-table plan (pass 2 in
+    # waves); the report does not change
+    c = configs.cfg3()
+    t = configs.load_targets(c)
+    cfg = MCConfig(paths=5000, seed=c.seed)
+    eng = Engine(c.spec)
+    base = eng.gradient_of_G(c.x, t, cfg)
+    assert eng.timing()["z_bytes"] > 0
+    eng.set_hbm_budget(1 << 20)
+    rep = eng.gradient_of_G(c.x, t, cfg)
+    assert eng.timing()["z_bytes"] == 0 and eng.timing()["ckpt_bytes"] == 0
+    assert rep.to_json() == base.to_json()
+    eng.set_hbm_budget(0)
+    eng.gradient_of_G(c.x, t, cfg)
+    assert eng.timing()["z_bytes"] > 0
+
+
 def test_nccl_attached_single_rank_bitwise():
     # the multi-GPU code path (run-time NCCL, in-place all-gather of the chunk
     # tables, all-reduce of the rare flag) on a one-rank communicator
