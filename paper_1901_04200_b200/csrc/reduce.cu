@@ -15,65 +15,102 @@
 namespace ltg {
 namespace {
 
-__global__ void reduce_groups_kernel(const double* __restrict__ table, uint64_t n_chunks,
-                                     uint32_t width, uint64_t n_groups,
-                                     double* __restrict__ groups) {
-    const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= n_groups * width) return;
-    const uint64_t g = idx / width;
-    const uint32_t col = (uint32_t)(idx % width);
+// Column sums of rows [r0, r1) of a row-major [*][width] table, each in
+// ascending row order (the fixed order the results depend on). The CTA
+// stages a kTileRows x tw tile through shared memory with independent,
+// coalesced loads, then thread t adds column t of the tile in row order, so a
+// column costs one memory latency per tile instead of one per row.
+constexpr int kTileRows = 64, kTileCols = 64;
+__device__ void ordered_column_sums(const double* table, uint64_t r0, uint64_t r1,
+                                    uint32_t width, double* out,
+                                    double (*tile)[kTileCols]) {
+    for (uint32_t c0 = 0; c0 < width; c0 += kTileCols) {
+        const uint32_t tw = min((uint32_t)kTileCols, width - c0);
+        double s = 0.0;
+        for (uint64_t rb = r0; rb < r1; rb += kTileRows) {
+            const uint32_t tr = (uint32_t)min((uint64_t)kTileRows, r1 - rb);
+            for (uint32_t e = threadIdx.x; e < tr * tw; e += blockDim.x) {
+                const uint32_t r = e / tw, c = e - r * tw;
+                tile[r][c] = table[(rb + r) * width + c0 + c];
+            }
+            __syncthreads();
+            if (threadIdx.x < tw)
+                for (uint32_t r = 0; r < tr; ++r) s = __dadd_rn(s, tile[r][threadIdx.x]);
+            __syncthreads();
+        }
+        if (threadIdx.x < tw) out[c0 + threadIdx.x] = s;
+    }
+}
+
+// one CTA per group of kGroup chunk rows
+__global__ void __launch_bounds__(kFinishThreads) reduce_groups_kernel(
+    const double* __restrict__ table, uint64_t n_chunks, uint32_t width,
+    double* __restrict__ groups) {
+    __shared__ double tile[kTileRows][kTileCols];
+    const uint64_t g = blockIdx.x;
     const uint64_t c0 = g * kGroup;
     const uint64_t c1 = min(c0 + (uint64_t)kGroup, n_chunks);
-    double s = 0.0;
-    for (uint64_t c = c0; c < c1; ++c) s += table[c * width + col];
-    groups[g * width + col] = s;
+    ordered_column_sums(table, c0, c1, width, groups + g * width, tile);
 }
 
-__global__ void reduce_final_kernel(const double* __restrict__ groups, uint64_t n_groups,
-                                    uint32_t width, double* __restrict__ out) {
-    const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
-    if (col >= width) return;
-    double s = 0.0;
-    for (uint64_t g = 0; g < n_groups; ++g) s += groups[g * width + col];
-    out[col] = s;
-}
-
-// means_from_sums (expectation.hpp:251-269) and lambda / G (:329-334)
-__global__ void finalize_means_kernel(const double* __restrict__ totals, uint32_t m,
-                                      uint64_t paths, const double* __restrict__ targets,
-                                      double* __restrict__ res) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// means_from_sums (expectation.hpp:251-269) for output o
+__device__ void finalize_mean(const double* totals, uint32_t m, uint64_t paths,
+                              const double* targets, double* res, uint32_t o) {
     const double P = (double)paths;
-    double* means = res + 1;
-    double* se = res + 1 + m;
-    double* lambda = res + 1 + 2 * m;
-    for (uint32_t o = 0; o < m; ++o) {
-        const double mean = __ddiv_rn(totals[o], P);
-        means[o] = mean;
-        if (paths > 1) {
-            double var = __ddiv_rn(__dsub_rn(totals[m + o], __dmul_rn(__dmul_rn(P, mean), mean)),
-                                   __dsub_rn(P, 1.0));
-            var = var > 0.0 ? var : 0.0;
-            se[o] = __dsqrt_rn(__ddiv_rn(var, P));
-        } else {
-            se[o] = 0.0;
-        }
+    const double mean = __ddiv_rn(totals[o], P);
+    res[1 + o] = mean;
+    if (paths > 1) {
+        double var = __ddiv_rn(__dsub_rn(totals[m + o], __dmul_rn(__dmul_rn(P, mean), mean)),
+                               __dsub_rn(P, 1.0));
+        var = var > 0.0 ? var : 0.0;
+        res[1 + m + o] = __dsqrt_rn(__ddiv_rn(var, P));
+    } else {
+        res[1 + m + o] = 0.0;
     }
-    double G = 0.0;
-    if (targets) {
-        for (uint32_t o = 0; o < m; ++o) {
-            const double l = __dsub_rn(means[o], targets[o]);
-            lambda[o] = l;
-            G = __dadd_rn(G, __dmul_rn(__dmul_rn(0.5, l), l));
-        }
-    }
-    res[0] = G;
+    if (targets) res[1 + 2 * m + o] = __dsub_rn(mean, targets[o]);  // lambda (:329-334)
 }
 
-__global__ void finalize_grad_kernel(const double* __restrict__ totals, uint32_t M,
-                                     uint64_t paths, double* __restrict__ grad) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < M) grad[j] = __ddiv_rn(totals[j], (double)paths);
+// Group sums -> totals (ascending group order), then the call's finishing
+// step in the same single-CTA launch:
+//   means: means, std errors, lambda per output (one thread each), then
+//          G = sum_o 0.5 * lambda_o^2 in ascending o (:329-334);
+//   grad:  grad = total / P (:340-342);
+//   grad_tangent: grad[d] = (sum_i lambda_i * J[i][d]) / P, i ascending,
+//          J = totals + 2m, lambda from res (written by `means` above when
+//          both are set).
+__global__ void __launch_bounds__(kFinishThreads) reduce_final_kernel(
+    const double* __restrict__ groups, uint64_t n_groups, uint32_t width, double* out, Finish f) {
+    __shared__ double tile[kTileRows][kTileCols];
+    ordered_column_sums(groups, 0, n_groups, width, out, tile);
+    if (!(f.means || f.grad || f.grad_tangent)) return;
+    __syncthreads();  // out visible to the block
+    if (f.means) {
+        for (uint32_t o = threadIdx.x; o < f.m; o += blockDim.x)
+            finalize_mean(out, f.m, f.paths, f.targets, f.res, o);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double G = 0.0;
+            if (f.targets) {
+                const double* lambda = f.res + 1 + 2 * f.m;
+                for (uint32_t o = 0; o < f.m; ++o)
+                    G = __dadd_rn(G, __dmul_rn(__dmul_rn(0.5, lambda[o]), lambda[o]));
+            }
+            f.res[0] = G;
+        }
+    }
+    if (f.grad)
+        for (uint32_t j = threadIdx.x; j < f.M; j += blockDim.x)
+            f.grad_out[j] = __ddiv_rn(out[j], (double)f.paths);
+    if (f.grad_tangent) {
+        const double* J = out + 2 * f.m;
+        const double* lambda = f.res + 1 + 2 * f.m;
+        for (uint32_t d = threadIdx.x; d < f.M; d += blockDim.x) {
+            double t = 0.0;
+            for (uint32_t i = 0; i < f.m; ++i)
+                t = __dadd_rn(t, __dmul_rn(lambda[i], J[(size_t)i * f.M + d]));
+            f.grad_out[d] = __ddiv_rn(t, (double)f.paths);
+        }
+    }
 }
 
 // PhiloxNormalSource::fill for a path range through the production
@@ -119,37 +156,15 @@ __global__ void inverse_normal_kernel(const RngTables* tables, RngConsts rc, con
     z[i] = fabs(q) <= rc.lit_qmax ? as241_central(q, rc) : as241_tail(q, sh, rc);
 }
 
-// tangent mode: grad[d] = (sum_i lambda_i * J[i*M + d]) / P, i ascending
-__global__ void finalize_grad_tangent_kernel(const double* J, const double* lambda, uint32_t m,
-                                             uint32_t M, uint64_t paths, double* grad) {
-    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
-    if (d >= M) return;
-    double t = 0.0;
-    for (uint32_t i = 0; i < m; ++i) t = __dadd_rn(t, __dmul_rn(lambda[i], J[(size_t)i * M + d]));
-    grad[d] = __ddiv_rn(t, (double)paths);
-}
-
 }  // namespace
 
 cudaError_t launch_reduce_chunks(const double* table, uint64_t n_chunks, uint32_t width,
-                                 double* group_scratch, double* out, cudaStream_t s) {
-    const uint64_t n_groups = (n_chunks + kGroup - 1) / kGroup;
-    const uint64_t n = n_groups * width;
-    reduce_groups_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(table, n_chunks, width,
-                                                                      n_groups, group_scratch);
-    reduce_final_kernel<<<(width + 127) / 128, 128, 0, s>>>(group_scratch, n_groups, width, out);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_finalize_means(const double* totals, uint32_t m, uint64_t paths,
-                                  const double* targets, double* res, cudaStream_t s) {
-    finalize_means_kernel<<<1, 32, 0, s>>>(totals, m, paths, targets, res);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_finalize_grad(const double* totals, uint32_t M, uint64_t paths, double* grad,
+                                 double* group_scratch, double* out, const Finish& fin,
                                  cudaStream_t s) {
-    finalize_grad_kernel<<<(M + 127) / 128, 128, 0, s>>>(totals, M, paths, grad);
+    const uint64_t n_groups = (n_chunks + kGroup - 1) / kGroup;
+    reduce_groups_kernel<<<(unsigned)n_groups, kFinishThreads, 0, s>>>(table, n_chunks, width,
+                                                                        group_scratch);
+    reduce_final_kernel<<<1, kFinishThreads, 0, s>>>(group_scratch, n_groups, width, out, fin);
     return cudaGetLastError();
 }
 
@@ -166,13 +181,6 @@ cudaError_t launch_inverse_normal(const RngTables* tables, const RngConsts& rc, 
                                    uint64_t n, double* z, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     inverse_normal_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(tables, rc, p, n, z);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_finalize_grad_tangent(const double* J, const double* lambda, uint32_t m,
-                                         uint32_t M, uint64_t paths, double* grad,
-                                         cudaStream_t s) {
-    finalize_grad_tangent_kernel<<<(M + 127) / 128, 128, 0, s>>>(J, lambda, m, M, paths, grad);
     return cudaGetLastError();
 }
 

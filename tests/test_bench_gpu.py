@@ -33,7 +33,7 @@ def test_engine_arm_json_contract():
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3
     assert d["dtype"] == "f64" and d["higher_is_better"] is True
     assert d["config"]["workload"] == "cfg3_heston"
-    assert d["gpu_launches"] == 2 * 8                  # 8 kernels per gradient_of_G
+    assert d["gpu_launches"] == 2 * 6                  # 6 kernels per gradient_of_G
     e = d["e2e"]
     assert e["unit"] == "paths/s" and 0 < e["value"] and e["h2d_bytes_per_step"] > 0
     r = d["roofline"]
