@@ -11,6 +11,7 @@ correlated baskets of 1-16 assets. Per case:
   * estimate_means (means and standard errors) and gradient_of_G within the
     1e-10 bar of test_gpu_parity.py;
   * a second call bitwise identical to the first;
+  * every 4th case: 2-5 loopback ranks on this GPU equal to one context;
   * tangent mode within the same bar where it applies (one column, <= 4 rows).
 Every 8th Heston case sits on an edge of the domain (V == 0, |rho| -> 1,
 heavy truncation, constant variance, a few hundred steps).
@@ -118,9 +119,29 @@ def test_random_heston_models(ref, case):
     z = ref.fill_normals(opts["seed"], prog.N, opts["antithetic"], path0, n)
     want = np.stack([prog.path_adjoint(x, z[i])[0] for i in range(n)])
     assert np.array_equal(y.view(np.uint64), want.view(np.uint64))
+    if case % 4 == 0:
+        _check_ranks(spec, x, opts, g)
+
+
+def _check_ranks(spec, x, opts, g):
+    # W loopback ranks on this GPU (test_gpu_parity.py::test_multi_rank_paths_on_one_gpu),
+    # W = 2..5, possibly more ranks than chunks: reports equal to one context's, bit for bit
+    import os
+    world = int(g.integers(2, 6))
+    os.environ["LTG_LOOPBACK"] = "1"
+    try:
+        grp = Engine(spec, devices=[0] * world)
+    finally:
+        os.environ.pop("LTG_LOOPBACK")
+    t = [1.0] * grp.m
+    cfg = MCConfig(paths=opts["paths"], seed=opts["seed"], antithetic=opts["antithetic"],
+                   fresh_step2_paths=opts["fresh"])
+    assert grp.gradient_of_G(x, t, cfg).to_json() == Engine(spec).gradient_of_G(x, t, cfg).to_json()
 
 
 @pytest.mark.parametrize("case", range(16))
 def test_random_baskets(ref, case):
     spec, x, opts, g = random_basket(2000 + case)
     _check(ref, spec, x, opts, g, False)
+    if case % 4 == 0:
+        _check_ranks(spec, x, opts, g)
