@@ -13,6 +13,10 @@
  *                          const MCConfig&)                 expectation.hpp:281-286
  *   ltg_finite_diff_gradient_of_G
  *                       <- lanetape::finite_diff_gradient_of_G   expectation.hpp:372-400
+ *   ltg_gradient_of_G_draws / ltg_estimate_means_draws
+ *                       <- the PathDrawSource overloads with BufferDrawSource /
+ *                          SampleSpace draws  expectation.hpp:274-279, 287-294,
+ *                          300-344, 354-367; rng.hpp:140-167
  *   ltg_fill_normals    <- lanetape::PhiloxNormalSource::fill    rng.hpp:113-127
  *   ltg_create_heston   <- lanetape::record_heston_program(ModelSpec) heston.hpp:327-329
  *                          (the GPU does not interpret tapes: the model description
@@ -46,7 +50,7 @@
 extern "C" {
 #endif
 
-#define LTG_ABI_VERSION 2
+#define LTG_ABI_VERSION 3
 
 #define LTG_OK 0
 #define LTG_EINVAL 1
@@ -204,6 +208,33 @@ int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_con
                        double* means, double* std_errors);
 int ltg_finite_diff_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
                                   size_t m, const ltg_mc_config* cfg, double h, double* grad);
+
+/* Caller-supplied draws: the reference's PathDrawSource overloads with a
+ * materialised source — BufferDrawSource (rng.hpp:140-167; also what
+ * BufferDrawSource::materialize makes of any user PathDrawSource) and
+ * SampleSpace (expectation.hpp:46-54, 85-101). Row p (dim doubles) holds the
+ * draws of path p, in the program's slot order (Heston: slot 2k drives V,
+ * 2k+1 the independent part of S; basket: slot k*n_assets + a). */
+typedef struct ltg_draws {
+    const double* data;          /* rows * dim, path-major, caller-owned */
+    uint64_t rows;
+    uint64_t dim;                /* must equal ltg_num_randoms (else LTG_EINVAL) */
+} ltg_draws;
+
+/* gradient_of_G(kernel, params, targets, src, cfg)   expectation.hpp:300-344
+ * with src = the caller's draws: pass 1 reads rows [0, paths), pass 2 the same
+ * rows, or rows [paths, 2*paths) with fresh_step2_paths. cfg->seed is only
+ * echoed into the report and cfg->antithetic is unused (the source fixes the
+ * draws), as in the reference. Too few rows -> LTG_EINVAL (the reference's
+ * std::out_of_range from fill). The SampleSpace overload (:354-367) is this
+ * call with rows = paths = scenarios, seed 0, recompute mode. */
+int ltg_gradient_of_G_draws(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
+                            size_t m, const ltg_draws* src, const ltg_mc_config* cfg,
+                            ltg_report* report);
+/* estimate_means(kernel, params, src, paths, workers)  expectation.hpp:274-279
+ * (and the SampleSpace overload :287-294 with paths = scenarios); fp64. */
+int ltg_estimate_means_draws(ltg_ctx* ctx, const double* x, size_t M, const ltg_draws* src,
+                             uint64_t paths, double* means, double* std_errors);
 
 /* One chunk of the two passes, unreduced (SURVEY §8(c) per-chunk parity):
  * over the global paths [path0, path0+npaths) of PhiloxNormalSource(seed),

@@ -79,6 +79,20 @@ struct GradientReport {
     std::uint64_t seed = 0;
 };
 
+// Draws fixed by the caller (rng.hpp:140-167 BufferDrawSource; a SampleSpace,
+// expectation.hpp:46-54, is the same rows with paths = scenarios): row p holds
+// the num_randoms() draws of path p.
+struct BufferDraws {
+    std::span<const double> draws;  // rows * dimension, path-major
+    std::size_t dimension = 0;
+};
+
+struct SampleSpace {
+    std::size_t scenarios = 0;
+    std::size_t num_randoms = 0;
+    std::vector<double> draws;  // scenario-major, scenarios * num_randoms
+};
+
 class EvalError : public std::runtime_error {
 public:
     using std::runtime_error::runtime_error;
@@ -191,6 +205,58 @@ public:
         return r;
     }
 
+    // gradient_of_G(kernel, params, targets, src, cfg) with a BufferDrawSource
+    // (expectation.hpp:300-344; ltg_gradient_of_G_draws): cfg.seed is echoed,
+    // cfg.antithetic unused; fresh_step2_paths reads rows [paths, 2*paths)
+    GradientReport gradient_of_G(std::span<const double> x, std::span<const double> targets,
+                                 const BufferDraws& src, const MCConfig& cfg) const {
+        GradientReport r;
+        r.means.resize(num_outputs());
+        r.lambda.resize(num_outputs());
+        r.grad.resize(num_params());
+        ltg_report rep{};
+        rep.means = r.means.data();
+        rep.lambda = r.lambda.data();
+        rep.grad = r.grad.data();
+        const ltg_mc_config c = detail::to_c(cfg);
+        const ltg_draws d = draws_of(src);
+        detail::check(ltg_gradient_of_G_draws(ctx_, x.data(), x.size(), targets.data(),
+                                              targets.size(), &d, &c, &rep),
+                      ltg_last_error(ctx_));
+        r.G = rep.G;
+        r.paths = rep.paths;
+        r.seed = rep.seed;
+        r.mode = rep.mode == LTG_MODE_STORE ? "store" : "recompute";
+        return r;
+    }
+
+    // the SampleSpace overload (expectation.hpp:354-367)
+    GradientReport gradient_of_G(std::span<const double> x, std::span<const double> targets,
+                                 const SampleSpace& space) const {
+        MCConfig cfg;
+        cfg.paths = space.scenarios;
+        cfg.seed = 0;
+        return gradient_of_G(x, targets, BufferDraws{space.draws, space.num_randoms}, cfg);
+    }
+
+    // estimate_means(kernel, params, src, paths) (expectation.hpp:274-279) and
+    // the SampleSpace overload (:287-294)
+    MeansResult estimate_means(std::span<const double> x, const BufferDraws& src,
+                               std::size_t paths) const {
+        MeansResult r;
+        r.means.resize(num_outputs());
+        r.std_errors.resize(num_outputs());
+        const ltg_draws d = draws_of(src);
+        detail::check(ltg_estimate_means_draws(ctx_, x.data(), x.size(), &d, paths,
+                                               r.means.data(), r.std_errors.data()),
+                      ltg_last_error(ctx_));
+        r.paths = paths;
+        return r;
+    }
+    MeansResult estimate_means(std::span<const double> x, const SampleSpace& space) const {
+        return estimate_means(x, BufferDraws{space.draws, space.num_randoms}, space.scenarios);
+    }
+
     // expectation.hpp:281-286
     MeansResult estimate_means(std::span<const double> x, const MCConfig& cfg) const {
         MeansResult r;
@@ -226,6 +292,13 @@ public:
     }
 
 private:
+    static ltg_draws draws_of(const BufferDraws& src) {
+        if (src.dimension == 0 || src.draws.size() % src.dimension != 0)
+            throw std::invalid_argument(
+                "BufferDrawSource: buffer size not a multiple of dimension");
+        return ltg_draws{src.draws.data(), src.draws.size() / src.dimension, src.dimension};
+    }
+
     ltg_ctx* ctx_ = nullptr;
 };
 

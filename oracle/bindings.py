@@ -190,6 +190,26 @@ class RefProgram:
             draws.size // self.N, lane_width, C.byref(G), _ptr(means), _ptr(lam), _ptr(grad)))
         return dict(G=G.value, means=means, lambda_=lam, grad=grad)
 
+    def gradient_of_G_buffer(self, x, targets, draws, paths, fresh=False, memory_mode=0,
+                             lane_width=8, workers=1):
+        """gradient_of_G(kernel, x, targets, BufferDrawSource(draws), cfg)"""
+        draws = _arr(draws)
+        G = C.c_double()
+        means, lam, grad = np.empty(self.m), np.empty(self.m), np.empty(self.M)
+        self._chk(self.ref.lib.ltref_gradient_of_G_buffer(
+            self.h, _ptr(_arr(x)), self.M, _ptr(_arr(targets)), self.m, _ptr(draws),
+            draws.size // self.N, paths, int(fresh), memory_mode, lane_width, workers,
+            C.byref(G), _ptr(means), _ptr(lam), _ptr(grad)))
+        return dict(G=G.value, means=means, lambda_=lam, grad=grad)
+
+    def estimate_means_buffer(self, x, draws, paths, lane_width=8, workers=1):
+        draws = _arr(draws)
+        means, se = np.empty(self.m), np.empty(self.m)
+        self._chk(self.ref.lib.ltref_estimate_means_buffer(
+            self.h, _ptr(_arr(x)), self.M, _ptr(draws), draws.size // self.N, paths, lane_width,
+            workers, _ptr(means), _ptr(se)))
+        return means, se
+
     def estimate_means(self, x, paths, seed, antithetic=False, lane_width=8, workers=1):
         means, se = np.empty(self.m), np.empty(self.m)
         self._chk(self.ref.lib.ltref_estimate_means(self.h, _ptr(_arr(x)), self.M, paths, seed,
@@ -265,6 +285,10 @@ class Ref:
         L.ltref_gradient_of_G_space.argtypes = [C.c_void_p, _dp, sz, _dp, sz, _dp, sz, i, _dp,
                                                 _dp, _dp, _dp]
         L.ltref_estimate_means.argtypes = [C.c_void_p, _dp, sz, u64, u64, i, i, i, _dp, _dp]
+        L.ltref_gradient_of_G_buffer.argtypes = [C.c_void_p, _dp, sz, _dp, sz, _dp, sz, u64, i,
+                                                 i, i, i, _dp, _dp, _dp, _dp]
+        L.ltref_estimate_means_buffer.argtypes = [C.c_void_p, _dp, sz, _dp, sz, u64, i, i, _dp,
+                                                  _dp]
         L.ltref_forward_sums.argtypes = [C.c_void_p, _dp, sz, u64, i, i, i, u64, u64, _dp, _dp]
         L.ltref_reverse_sums.argtypes = [C.c_void_p, _dp, sz, u64, i, i, i, u64, u64, _dp, sz,
                                          _dp]

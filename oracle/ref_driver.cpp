@@ -269,6 +269,44 @@ int ltref_gradient_of_G_space(void* prog, const double* x, size_t M, const doubl
     });
 }
 
+// gradient_of_G(Kernel, params, targets, PathDrawSource, cfg) with a
+// BufferDrawSource over the caller's path-major rows (expectation.hpp:300-344,
+// rng.hpp:140-167): the reference side of ltg_gradient_of_G_draws
+int ltref_gradient_of_G_buffer(void* prog, const double* x, size_t M, const double* C, size_t m,
+                               const double* draws, size_t rows, uint64_t paths, int fresh,
+                               int memory_mode, int lane_width, int workers, double* G,
+                               double* means, double* lambda, double* grad) {
+    return guarded([&] {
+        auto* p = static_cast<Program*>(prog);
+        const size_t dim = p->tape.num_randoms();
+        BufferDrawSource src(std::vector<double>(draws, draws + rows * dim), dim);
+        MCConfig cfg = make_cfg(paths, 0, 0, lane_width, workers, memory_mode, fresh);
+        Kernel k = Kernel::freeze(p->tape, lane_width);
+        auto rep = gradient_of_G(k, std::span<const double>(x, M), std::span<const double>(C, m),
+                                 src, cfg);
+        *G = rep.G;
+        std::copy(rep.means.begin(), rep.means.end(), means);
+        std::copy(rep.lambda.begin(), rep.lambda.end(), lambda);
+        std::copy(rep.grad.begin(), rep.grad.end(), grad);
+    });
+}
+
+// estimate_means(Kernel, params, PathDrawSource, paths, workers) over a
+// BufferDrawSource (expectation.hpp:274-279)
+int ltref_estimate_means_buffer(void* prog, const double* x, size_t M, const double* draws,
+                                size_t rows, uint64_t paths, int lane_width, int workers,
+                                double* means, double* se) {
+    return guarded([&] {
+        auto* p = static_cast<Program*>(prog);
+        const size_t dim = p->tape.num_randoms();
+        BufferDrawSource src(std::vector<double>(draws, draws + rows * dim), dim);
+        Kernel k = Kernel::freeze(p->tape, lane_width);
+        auto r = estimate_means(k, std::span<const double>(x, M), src, paths, workers);
+        std::copy(r.means.begin(), r.means.end(), means);
+        if (se) std::copy(r.std_errors.begin(), r.std_errors.end(), se);
+    });
+}
+
 int ltref_estimate_means(void* prog, const double* x, size_t M, uint64_t paths, uint64_t seed,
                          int antithetic, int lane_width, int workers, double* means, double* se) {
     return guarded([&] {

@@ -55,6 +55,11 @@ class MCConfigC(C.Structure):
     ]
 
 
+class DrawsC(C.Structure):
+    """ltg_draws: caller draws, path-major rows of dim doubles"""
+    _fields_ = [("data", C.POINTER(C.c_double)), ("rows", C.c_uint64), ("dim", C.c_uint64)]
+
+
 class ReportC(C.Structure):
     _fields_ = [
         ("G", C.c_double),

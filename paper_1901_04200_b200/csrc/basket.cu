@@ -126,10 +126,11 @@ __device__ inline void bflush(double* acc, uint32_t width, double* row, Map map)
 // is called with the event index. SAFE = false uses glibc exp's main path
 // without the |x| >= 512 guard and raises the path's rare flag instead (the
 // host then reruns the call with SAFE = true; see heston.cu heston_step).
-template <bool TRACK_W, bool SAFE, int NAT, typename Visit>
+template <bool TRACK_W, bool SAFE, int NAT, bool DRAWS, typename Visit>
 __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, const Work& w,
-                                         uint64_t base, bool neg, double (&S)[NA],
-                                         double (&W)[NA], unsigned& chk, Visit visit) {
+                                         uint64_t base, bool neg, const double* drow, bool valid,
+                                         double (&S)[NA], double (&W)[NA], unsigned& chk,
+                                         Visit visit) {
     const int tid = threadIdx.x, warp = tid >> 5;
     double* zb = s.zbuf + tid;
     uint16_t* wl = s.list + warp * 64 * BGS;
@@ -145,7 +146,11 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
         const uint32_t nb = min(2u, a.steps - k0);
         const uint32_t pair0 = (k0 * n) >> 1;
         const int npairs = (int)((nb * n + 1) >> 1);
-        gen_segment<BGS>(base, neg, pair0, npairs, w.seed_lo, w.seed_hi, zb, wl, *s.tab, a.rc);
+        if (DRAWS)  // caller draws: slots [k0*n, k0*n + 2*npairs) of the path's row
+            copy_draws<double>(drow, valid, 2 * pair0, 2 * npairs, a.steps * n, zb);
+        else
+            gen_segment<BGS>(base, neg, pair0, npairs, w.seed_lo, w.seed_hi, zb, wl, *s.tab,
+                             a.rc);
         for (uint32_t j = 0; j < nb; ++j) {
             const uint32_t k = k0 + j;
             double z[NA];
@@ -184,7 +189,7 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
 constexpr unsigned kBRareThr = 0x7ca00000u;
 
 // NAT = 16 (config 4) specialises the asset loops; NAT = 0 takes a.n at run time
-template <bool SAFE, int NAT>
+template <bool SAFE, int NAT, bool DRAWS = false>
 __global__ void __launch_bounds__(kBlock, 4) basket_pass1_kernel(BasketArgs a, Work w) {
     extern __shared__ __align__(16) char smem_raw[];
     __shared__ uint32_t chunk_slot;
@@ -229,10 +234,13 @@ __global__ void __launch_bounds__(kBlock, 4) basket_pass1_kernel(BasketArgs a, W
                     }
                 }
             };
+            const double* drow = DRAWS ? a.draws + (base - a.draws_row0) * ((uint64_t)a.steps * n)
+                                       : nullptr;
             if (a.write_store)
-                simulate<true, SAFE, NAT>(a, s, w, base, neg, S, W, chk, visit);
+                simulate<true, SAFE, NAT, DRAWS>(a, s, w, base, neg, drow, valid, S, W, chk, visit);
             else
-                simulate<false, SAFE, NAT>(a, s, w, base, neg, S, W, chk, visit);
+                simulate<false, SAFE, NAT, DRAWS>(a, s, w, base, neg, drow, valid, S, W, chk,
+                                                  visit);
             if (chk >= kBRareThr && valid) atomicOr(a.rare, 1u);
         }
         if (a.write_sums) {
@@ -256,7 +264,7 @@ __device__ __forceinline__ double contribution(const BasketArgs& a, const BSmem&
     return lam * Sa * (a.sqdt * Wa - a.sigma[c] * a.dt * (double)ms);
 }
 
-template <bool SAFE, int NAT>
+template <bool SAFE, int NAT, bool DRAWS = false>
 __global__ void __launch_bounds__(kBlock, 4) basket_pass2_kernel(BasketArgs a, Work w) {
     extern __shared__ __align__(16) char smem_raw[];
     __shared__ uint32_t chunk_slot;
@@ -292,7 +300,9 @@ __global__ void __launch_bounds__(kBlock, 4) basket_pass2_kernel(BasketArgs a, W
                 const bool neg = w.antithetic && (path & 1u);
                 double S[NA], W[NA];
                 unsigned chk = 0;
-                simulate<true, SAFE, NAT>(a, s, w, base, neg, S, W, chk,
+                const double* drow =
+                    DRAWS ? a.draws + (base - a.draws_row0) * ((uint64_t)a.steps * n) : nullptr;
+                simulate<true, SAFE, NAT, DRAWS>(a, s, w, base, neg, drow, valid, S, W, chk,
                                      [&](uint32_t ev, uint32_t ms) {
                     const MaturityEvent e = a.events[ev];
                     for (uint32_t pos = e.begin; pos < e.end; ++pos) {
@@ -323,6 +333,11 @@ cudaError_t blaunch(K kernel, const BasketArgs& a, const Work& w, int grid, size
 
 cudaError_t launch_basket_pass1(const BasketArgs& a, const Work& w, int grid, cudaStream_t st) {
     const size_t smem = basket_smem(a.m, 2 * a.m);
+    if (a.draws)  // caller draws: exact slow paths only (the host runs safe)
+        return !a.safe ? cudaErrorInvalidValue
+               : a.n == kMaxAssets
+                   ? blaunch(basket_pass1_kernel<true, kMaxAssets, true>, a, w, grid, smem, st)
+                   : blaunch(basket_pass1_kernel<true, 0, true>, a, w, grid, smem, st);
     if (a.n == kMaxAssets)
         return a.safe ? blaunch(basket_pass1_kernel<true, kMaxAssets>, a, w, grid, smem, st)
                       : blaunch(basket_pass1_kernel<false, kMaxAssets>, a, w, grid, smem, st);
@@ -332,6 +347,11 @@ cudaError_t launch_basket_pass1(const BasketArgs& a, const Work& w, int grid, cu
 
 cudaError_t launch_basket_pass2(const BasketArgs& a, const Work& w, int grid, cudaStream_t st) {
     const size_t smem = basket_smem(a.m, a.n);
+    if (a.draws)
+        return !a.safe ? cudaErrorInvalidValue
+               : a.n == kMaxAssets
+                   ? blaunch(basket_pass2_kernel<true, kMaxAssets, true>, a, w, grid, smem, st)
+                   : blaunch(basket_pass2_kernel<true, 0, true>, a, w, grid, smem, st);
     if (a.n == kMaxAssets)
         return a.safe ? blaunch(basket_pass2_kernel<true, kMaxAssets>, a, w, grid, smem, st)
                       : blaunch(basket_pass2_kernel<false, kMaxAssets>, a, w, grid, smem, st);

@@ -221,6 +221,12 @@ struct ltg_ctx {
     DevBuf d_x, d_targets, d_part1, d_part2, d_groups, d_tot1, d_tot2, d_res, d_grad, d_counter,
         d_ckpt, d_ztab, d_normals;
     uint64_t z_chunks = 0;  // leading local chunks whose draws pass 1 stored
+    // caller-supplied draws of the current *_draws call (DrawScope): rows
+    // [row0A, row0A + rowsA) of the caller's buffer for pass 1, then, with
+    // fresh_step2_paths, rows [row0B, row0B + rowsA) for pass 2
+    DevBuf d_draws;
+    bool draws_on = false;
+    uint64_t draws_rowsA = 0, draws_row0A = 0, draws_row0B = 0;
     // inputs and outcome of the last HBM plan (run_pass1); a call with the
     // same inputs reuses it without querying the device (its buffers are held)
     std::string plan_key;
@@ -434,6 +440,10 @@ BasketArgs basket_args(ltg_ctx* c, const double* x) {
     a.rc = c->h_rc;
     a.safe = c->safe;
     a.rare = c->d_counter.as<uint32_t>() + kRareSlot;
+    if (c->draws_on) {
+        a.draws = c->d_draws.as<double>();
+        a.draws_row0 = c->draws_row0A;
+    }
     return a;
 }
 
@@ -483,6 +493,10 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
     a.fp32 = c->fp32;
     a.safe = c->safe;
     a.rare = c->d_counter.as<uint32_t>() + kRareSlot;
+    if (c->draws_on) {
+        a.draws = c->d_draws.as<double>();
+        a.draws_row0 = c->draws_row0A;
+    }
     return a;
 }
 
@@ -498,7 +512,9 @@ Work base_work(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan) {
     w.counter = c->d_counter.as<uint32_t>();
     w.seed_lo = (uint32_t)cfg.seed;
     w.seed_hi = (uint32_t)(cfg.seed >> 32);
-    w.antithetic = cfg.antithetic ? 1 : 0;
+    // (caller draws: no antithetic pairing, so the kernels' Philox path word
+    // is the path index, which also addresses the caller's row)
+    w.antithetic = cfg.antithetic && !c->draws_on ? 1 : 0;
     return w;
 }
 
@@ -581,7 +597,8 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                   std::to_string(plan.chunk_paths) + "/" + std::to_string(w.ckpt_stride) + "/" +
                   std::to_string(c->fp32) + "/" + std::to_string(c->hbm_budget) + "/" +
                   env_or("LTG_HBM_BUDGET_GB") + "/" + env_or("LTG_CKPT_STEPS") + "/" +
-                  env_or("LTG_ZSTORE") + "/" + env_or("LTG_ZCHUNKS_MAX")
+                  env_or("LTG_ZSTORE") + "/" + env_or("LTG_ZCHUNKS_MAX") + "/" +
+                  std::to_string(c->draws_on ? 1 : 0)
             : std::string();
     if (!key.empty() && key == c->plan_key) {
         c->seg_steps = c->plan_ks;
@@ -608,7 +625,8 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         };
         const char* env_ks = std::getenv("LTG_CKPT_STEPS");
         const char* env_z = std::getenv("LTG_ZSTORE");
-        const bool z_ok = !(env_z && env_z[0] == '0');
+        // (caller draws: pass 2 reads the caller's rows, nothing to store)
+        const bool z_ok = !(env_z && env_z[0] == '0') && !c->draws_on;
         const uint32_t forced = env_ks ? (uint32_t)std::atoi(env_ks) : 0u;
         // the first interval whose checkpoint table fits, with the draws of as
         // many chunks as the rest of HBM holds (KS = 8 halves the replay
@@ -693,12 +711,18 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     c->d_grad.ensure(c->M * 8);
     HestonArgs a = heston_args(c, c->h_x.data());
     a.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
+    if (c->draws_on && cfg.fresh_step2_paths) {  // the caller rows of the fresh path set
+        a.draws = c->d_draws.as<double>() + c->draws_rowsA * c->N;
+        a.draws_row0 = c->draws_row0B;
+    }
     Work w = base_work(c, cfg, plan);
     const uint32_t nseg = (c->steps + c->seg_steps - 1) / c->seg_steps;
     cuda_check(cudaEventRecord(c->ev[3], c->stream), "event");
     if (w.n_chunks && c->kind == 1) {
         BasketArgs b = basket_args(c, c->h_x.data());
         b.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
+        b.draws = a.draws;
+        b.draws_row0 = a.draws_row0;
         b.partials = c->d_part2.as<double>() + plan.chunk_begin * c->M;
         b.use_store = have_ckpt && !cfg.fresh_step2_paths ? 1 : 0;
         b.store = b.use_store ? c->d_ckpt.as<double2>() : nullptr;
@@ -1147,13 +1171,75 @@ int ltg_shard_plan(uint64_t paths, int rank, int world, ltg_shard* out) {
 
 namespace {
 
+// Caller-supplied draws for one call (ltg_*_draws): validates the source as
+// the reference does (forward_pass's dimension check, expectation.hpp:156-159;
+// BufferDrawSource / SampleSpaceSource's row bound, rng.hpp:160-161,
+// expectation.hpp:92-94, raised here before any launch instead of mid-pass),
+// uploads this rank's rows (and those of the fresh step-2 path set) and
+// releases them when the call ends, so the Philox calls' HBM plan keeps the
+// memory.
+struct DrawScope {
+    ltg_ctx* c = nullptr;
+    DrawScope(ltg_ctx* ctx, const ltg_draws* src, const ltg_mc_config& cfg,
+              const ltg_shard& plan) {
+        if (!src) return;
+        require(src->data != nullptr, "null draw buffer");
+        require(cfg.precision == LTG_FP64, "caller draws: fp64 only (the reference's arithmetic)");
+        require(src->dim == ctx->N, "forward_pass: draw source dimension " +
+                                        std::to_string(src->dim) + " != tape randoms " +
+                                        std::to_string(ctx->N));
+        require(src->rows <= (uint64_t(1) << 62) / std::max<uint64_t>(1, src->dim),
+                "draw buffer size overflows");
+        const uint64_t need_rows = cfg.fresh_step2_paths ? 2 * cfg.paths : cfg.paths;
+        require(src->rows >= need_rows,
+                "BufferDrawSource: path index out of range (" + std::to_string(need_rows) +
+                    " paths need draws, the buffer has " + std::to_string(src->rows) + ")");
+        c = ctx;
+        const uint64_t rows = plan.path_end - plan.path_begin;
+        const uint64_t n_regions = cfg.fresh_step2_paths ? 2 : 1;
+        const size_t row_bytes = size_t(ctx->N) * 8;
+        const size_t need = std::max<size_t>(8, size_t(rows * n_regions) * row_bytes);
+        if (need > ctx->d_draws.bytes) {
+            // a previous Philox call's draw store may hold the free HBM
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            if (need + (size_t(1) << 30) > free_b) {
+                ctx->d_ztab.release();
+                ctx->plan_key.clear();
+            }
+            ctx->d_draws.ensure(need);
+        }
+        if (rows) {
+            cuda_check(cudaMemcpyAsync(ctx->d_draws.p, src->data + plan.path_begin * ctx->N,
+                                       rows * row_bytes, cudaMemcpyHostToDevice, ctx->stream),
+                       "H2D draws");
+            if (cfg.fresh_step2_paths)
+                cuda_check(cudaMemcpyAsync(ctx->d_draws.as<double>() + rows * ctx->N,
+                                           src->data + (cfg.paths + plan.path_begin) * ctx->N,
+                                           rows * row_bytes, cudaMemcpyHostToDevice, ctx->stream),
+                           "H2D draws");
+        }
+        ctx->draws_on = true;
+        ctx->draws_rowsA = rows;
+        ctx->draws_row0A = plan.path_begin;
+        ctx->draws_row0B = cfg.paths + plan.path_begin;
+    }
+    ~DrawScope() {
+        if (!c) return;
+        c->draws_on = false;
+        cudaStreamSynchronize(c->stream);
+        c->d_draws.release();
+    }
+};
+
 int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets, size_t m,
-                  const ltg_mc_config* cfg, ltg_report* report, bool tangent) {
+                  const ltg_mc_config* cfg, ltg_report* report, bool tangent,
+                  const ltg_draws* src = nullptr) {
     if (!ctx) return LTG_EINVAL;
     if (is_group(ctx)) {
         const ltg_report proto = report ? *report : ltg_report{};
         return group_run(ctx, [&](ltg_ctx* mb, size_t i) {
-            if (i == 0) return gradient_impl(mb, x, M, targets, m, cfg, report, tangent);
+            if (i == 0) return gradient_impl(mb, x, M, targets, m, cfg, report, tangent, src);
             // the other ranks' identical reports land in scratch (same nullness,
             // so every member validates alike)
             std::vector<double> means(ctx->m), lambda(ctx->m), grad(ctx->M), se(ctx->m);
@@ -1162,7 +1248,7 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
             r.lambda = proto.lambda ? lambda.data() : nullptr;
             r.grad = proto.grad ? grad.data() : nullptr;
             r.std_errors = proto.std_errors ? se.data() : nullptr;
-            return gradient_impl(mb, x, M, targets, m, cfg, report ? &r : nullptr, tangent);
+            return gradient_impl(mb, x, M, targets, m, cfg, report ? &r : nullptr, tangent, src);
         });
     }
     return guarded(ctx, [&] {
@@ -1181,10 +1267,12 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
                     "most 4 leverage rows (M <= 9); use ltg_gradient_of_G");
         check_params(ctx, x);
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
+        const DrawScope draws(ctx, src, *cfg, plan);
         const uint32_t nm = ctx->m;
         double* st = nullptr;
-        for (ctx->safe = start_safe(ctx);; ctx->safe = 1) {
-            const uint32_t rerun = ctx->safe && !start_safe(ctx) ? 1u : 0u;
+        // (caller draws run the exact slow paths from the start: DrawScope)
+        for (ctx->safe = src ? 1 : start_safe(ctx);; ctx->safe = 1) {
+            const uint32_t rerun = ctx->safe && !src && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
             ctx->timing.safe_rerun = rerun;
             upload_x(ctx, x, targets);
@@ -1240,6 +1328,16 @@ int ltg_gradient_of_G_tangent(ltg_ctx* ctx, const double* x, size_t M, const dou
     return gradient_impl(ctx, x, M, targets, m, cfg, report, true);
 }
 
+int ltg_gradient_of_G_draws(ltg_ctx* ctx, const double* x, size_t M, const double* targets,
+                            size_t m, const ltg_draws* src, const ltg_mc_config* cfg,
+                            ltg_report* report) {
+    if (!src) {
+        if (ctx && !is_group(ctx)) ctx->err = "null draw source";
+        return LTG_EINVAL;
+    }
+    return gradient_impl(ctx, x, M, targets, m, cfg, report, false, src);
+}
+
 int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda, size_t m,
                    uint64_t seed, int antithetic, uint64_t path0, uint64_t npaths,
                    double* sums, double* sumsq, double* adjoint) {
@@ -1291,25 +1389,29 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
     });
 }
 
-int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg,
-                       double* means, double* std_errors) {
+namespace {
+
+int means_impl(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg,
+               double* means, double* std_errors, const ltg_draws* src) {
     if (!ctx) return LTG_EINVAL;
     if (is_group(ctx))
         return group_run(ctx, [&](ltg_ctx* mb, size_t i) {
-            if (i == 0) return ltg_estimate_means(mb, x, M, cfg, means, std_errors);
+            if (i == 0) return means_impl(mb, x, M, cfg, means, std_errors, src);
             std::vector<double> mv(ctx->m), sv(ctx->m);
-            return ltg_estimate_means(mb, x, M, cfg, means ? mv.data() : nullptr,
-                                      std_errors ? sv.data() : nullptr);
+            return means_impl(mb, x, M, cfg, means ? mv.data() : nullptr,
+                              std_errors ? sv.data() : nullptr, src);
         });
     return guarded(ctx, [&] {
         validate_cfg(ctx, cfg, M);
         require(x && means, "null buffer");
         check_params(ctx, x);
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
+        const DrawScope draws(ctx, src, *cfg, plan);
         const uint32_t nm = ctx->m;
         double* st = nullptr;
-        for (ctx->safe = start_safe(ctx);; ctx->safe = 1) {
-            const uint32_t rerun = ctx->safe && !start_safe(ctx) ? 1u : 0u;
+        // (caller draws run the exact slow paths from the start: DrawScope)
+        for (ctx->safe = src ? 1 : start_safe(ctx);; ctx->safe = 1) {
+            const uint32_t rerun = ctx->safe && !src && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
             ctx->timing.safe_rerun = rerun;
             upload_x(ctx, x, nullptr);
@@ -1331,6 +1433,25 @@ int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_con
             if (!std::isfinite(means[o]))
                 throw Failure(LTG_ENUMERIC, "estimate_means: non-finite result");
     });
+}
+
+}  // namespace
+
+int ltg_estimate_means(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg,
+                       double* means, double* std_errors) {
+    return means_impl(ctx, x, M, cfg, means, std_errors, nullptr);
+}
+
+int ltg_estimate_means_draws(ltg_ctx* ctx, const double* x, size_t M, const ltg_draws* src,
+                             uint64_t paths, double* means, double* std_errors) {
+    if (!src) {
+        if (ctx && !is_group(ctx)) ctx->err = "null draw source";
+        return LTG_EINVAL;
+    }
+    // estimate_means(Kernel, params, PathDrawSource, paths, workers): fp64, no
+    // seed or antithetic pairing (the source fixes the draws)
+    const ltg_mc_config cfg{paths, 0, 0, 0, LTG_MODE_RECOMPUTE, LTG_FP64};
+    return means_impl(ctx, x, M, &cfg, means, std_errors, src);
 }
 
 int ltg_finite_diff_gradient_of_G(ltg_ctx* ctx, const double* x, size_t M, const double* targets,

@@ -16,9 +16,10 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import cabi
-from .cabi import (LTG_ECUDA, LTG_EINVAL, LTG_ENUMERIC, MarshalledModel, MCConfigC, ReportC,
-                   ShardC, TimingC)
-from .model import GradientReport, MCConfig, MeansResult, memory_mode_name
+from .cabi import (LTG_ECUDA, LTG_EINVAL, LTG_ENUMERIC, DrawsC, MarshalledModel, MCConfigC,
+                   ReportC, ShardC, TimingC)
+from .model import (BufferDrawSource, GradientReport, MCConfig, MeansResult, SampleSpace,
+                    memory_mode_name)
 
 LIB_PATH = os.environ.get("LTG_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_lib", "liblanetape_b200.so")
@@ -61,6 +62,11 @@ def load_library(path: str = LIB_PATH):
                                     C.POINTER(MCConfigC), C.POINTER(ReportC)]
     L.ltg_gradient_of_G_tangent.argtypes = L.ltg_gradient_of_G.argtypes
     L.ltg_estimate_means.argtypes = [C.c_void_p, _dp, C.c_size_t, C.POINTER(MCConfigC), _dp, _dp]
+    L.ltg_gradient_of_G_draws.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, C.c_size_t,
+                                          C.POINTER(DrawsC), C.POINTER(MCConfigC),
+                                          C.POINTER(ReportC)]
+    L.ltg_estimate_means_draws.argtypes = [C.c_void_p, _dp, C.c_size_t, C.POINTER(DrawsC),
+                                           C.c_uint64, _dp, _dp]
     L.ltg_finite_diff_gradient_of_G.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, C.c_size_t,
                                                 C.POINTER(MCConfigC), C.c_double, _dp]
     L.ltg_fill_normals.argtypes = [C.c_void_p, C.c_uint64, C.c_size_t, C.c_int, C.c_uint64,
@@ -195,20 +201,49 @@ class Engine:
         self.lib.ltg_pack_params(self.h, _p(x), self.M)
         return x
 
-    def gradient_of_G(self, x, targets, cfg: MCConfig, std_errors: bool = False,
-                      method: str = "adjoint") -> GradientReport:
-        """expectation.hpp:346-351. method="adjoint" is the reference's two-pass
-        scheme; "tangent" replaces pass 2 by pathwise forward tangents
-        (ltg_gradient_of_G_tangent: small-M Heston models only)."""
+    @staticmethod
+    def _draws(source):
+        """(ltg_draws, keep-alive array) of a BufferDrawSource / SampleSpace"""
+        if isinstance(source, SampleSpace):
+            buf = np.ascontiguousarray(source.draws, dtype=np.float64).ravel()
+            if buf.size != source.scenarios * source.num_randoms:
+                raise ValueError("SampleSpace: draws size does not match dimensions")
+            return DrawsC(_p(buf), source.scenarios, source.num_randoms), buf
+        if isinstance(source, BufferDrawSource):
+            return DrawsC(_p(source.draws), source.paths(), source.dimension()), source.draws
+        raise TypeError("source must be a BufferDrawSource or a SampleSpace")
+
+    def gradient_of_G(self, x, targets, cfg, std_errors: bool = False,
+                      method: str = "adjoint", source=None) -> GradientReport:
+        """expectation.hpp:346-351 (Philox draws from cfg.seed). method="adjoint"
+        is the reference's two-pass scheme; "tangent" replaces pass 2 by
+        pathwise forward tangents (ltg_gradient_of_G_tangent: small-M Heston
+        models only).
+
+        The reference's other overloads (ltg_gradient_of_G_draws):
+        ``source=BufferDrawSource`` is gradient_of_G(kernel, params, targets,
+        src, cfg) (:300-344); ``cfg=SampleSpace`` is the scenario-set overload
+        (:354-367: paths = scenarios, seed 0, recompute)."""
         xa, ta = _arr(x), _arr(targets)
         means, lam, grad = np.empty(self.m), np.empty(self.m), np.empty(self.M)
         se = np.empty(self.m) if std_errors else None
         rep = ReportC(0.0, _p(means), _p(lam), _p(grad), _p(se), 0, 0, 0)
-        c = _cfg(cfg)
         if method not in ("adjoint", "tangent"):
             raise ValueError(f"unknown method {method!r}")
-        fn = self.lib.ltg_gradient_of_G if method == "adjoint" else self.lib.ltg_gradient_of_G_tangent
-        rc = fn(self.h, _p(xa), xa.size, _p(ta), ta.size, C.byref(c), C.byref(rep))
+        if isinstance(cfg, SampleSpace):
+            source, cfg = cfg, MCConfig(paths=cfg.scenarios, seed=0)
+        c = _cfg(cfg)
+        if source is not None:
+            if method != "adjoint":
+                raise ValueError("caller draws: method='adjoint' only")
+            d, keep = self._draws(source)
+            rc = self.lib.ltg_gradient_of_G_draws(self.h, _p(xa), xa.size, _p(ta), ta.size,
+                                                  C.byref(d), C.byref(c), C.byref(rep))
+            del keep
+        else:
+            fn = (self.lib.ltg_gradient_of_G if method == "adjoint"
+                  else self.lib.ltg_gradient_of_G_tangent)
+            rc = fn(self.h, _p(xa), xa.size, _p(ta), ta.size, C.byref(c), C.byref(rep))
         if rc:
             self._raise(rc)
         out = GradientReport(rep.G, means.tolist(), lam.tolist(), grad.tolist(), int(rep.paths),
@@ -217,15 +252,30 @@ class Engine:
             out.std_errors = se.tolist()
         return out
 
-    def estimate_means(self, x, cfg: MCConfig) -> MeansResult:
-        """expectation.hpp:281-286"""
+    def estimate_means(self, x, cfg, source=None, paths: Optional[int] = None) -> MeansResult:
+        """expectation.hpp:281-286 (Philox draws from cfg.seed); with
+        ``source=BufferDrawSource`` and ``paths`` the PathDrawSource overload
+        (:274-279), with ``cfg=SampleSpace`` the scenario-set overload
+        (:287-294) — both through ltg_estimate_means_draws."""
         xa = _arr(x)
         means, se = np.empty(self.m), np.empty(self.m)
-        c = _cfg(cfg)
-        rc = self.lib.ltg_estimate_means(self.h, _p(xa), xa.size, C.byref(c), _p(means), _p(se))
+        if isinstance(cfg, SampleSpace):
+            source, paths = cfg, cfg.scenarios
+        if source is not None:
+            if paths is None:
+                raise ValueError("estimate_means with a draw source needs paths")
+            d, keep = self._draws(source)
+            rc = self.lib.ltg_estimate_means_draws(self.h, _p(xa), xa.size, C.byref(d), paths,
+                                                   _p(means), _p(se))
+            del keep
+        else:
+            paths = cfg.paths
+            c = _cfg(cfg)
+            rc = self.lib.ltg_estimate_means(self.h, _p(xa), xa.size, C.byref(c), _p(means),
+                                             _p(se))
         if rc:
             self._raise(rc)
-        return MeansResult(means.tolist(), se.tolist(), int(cfg.paths))
+        return MeansResult(means.tolist(), se.tolist(), int(paths))
 
     def finite_diff_gradient_of_G(self, x, targets, cfg: MCConfig, h: float) -> np.ndarray:
         """expectation.hpp:372-400"""

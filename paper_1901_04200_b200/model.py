@@ -233,6 +233,48 @@ class MCConfig:
     precision: int = FP64
 
 
+@dataclass
+class SampleSpace:
+    """expectation.hpp:46-54: an explicit, uniformly weighted scenario set
+    (scenario-major draws, scenarios * num_randoms)."""
+    scenarios: int = 0
+    num_randoms: int = 0
+    draws: Sequence[float] = field(default_factory=list)
+
+    def row(self, s: int) -> Sequence[float]:
+        return self.draws[s * self.num_randoms:(s + 1) * self.num_randoms]
+
+
+class BufferDrawSource:
+    """rng.hpp:140-167: draws read from a flat path-major buffer (row p = the
+    `dimension` draws of path p)."""
+
+    def __init__(self, draws, dimension: int):
+        import numpy as np
+        self.draws = np.ascontiguousarray(draws, dtype=np.float64).ravel()
+        self.dim = int(dimension)
+        if self.dim == 0 or self.draws.size % self.dim != 0:
+            raise ValueError("BufferDrawSource: buffer size not a multiple of dimension")
+
+    @staticmethod
+    def materialize(fill, dimension: int, paths: int) -> "BufferDrawSource":
+        """rng.hpp:149-154 for a source given as fill(path0, npaths) -> the
+        path-major draws of paths [path0, path0 + npaths), e.g.
+        ``lambda p0, n: engine.fill_normals(seed, dim, anti, p0, n)``."""
+        return BufferDrawSource(fill(0, paths), dimension)
+
+    def dimension(self) -> int:
+        return self.dim
+
+    def paths(self) -> int:
+        return self.draws.size // self.dim
+
+    def fill(self, path: int):
+        if path >= self.paths():
+            raise IndexError("BufferDrawSource: path index out of range")
+        return self.draws[path * self.dim:(path + 1) * self.dim]
+
+
 def memory_mode_name(m: int) -> str:
     """expectation.hpp:19-21"""
     return "store" if m == MODE_STORE else "recompute"

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert engine.load_library().ltg_abi_version() == 2
+    assert engine.load_library().ltg_abi_version() == 3
 
 
 def test_rng_log_restatement_matches_host_libm():
