@@ -1,5 +1,5 @@
 """Small calls that launch every kernel variant of the engine at least once
-(development check; `python tools/sanitize_cases.py` exits non-zero on any
+(development check; `python tools/every_variant.py` exits non-zero on any
 engine error). Written for compute-sanitizer, which this GPU pool does not
 allow; the variants' results are covered by the parity suites.
 
