@@ -10,7 +10,8 @@ correlated baskets of 1-16 assets. Per case:
     (path_adjoint) on its own PhiloxNormalSource draws (Heston);
   * estimate_means (means and standard errors) and gradient_of_G within the
     1e-10 bar of test_gpu_parity.py;
-  * a second call bitwise identical to the first;
+  * a second call bitwise identical to the first, and the same call on the
+    materialised draws (ltg_gradient_of_G_draws) bitwise identical too;
   * every 4th case: 2-5 loopback ranks on this GPU equal to one context;
   * tangent mode within the same bar where it applies (one column, <= 4 rows).
 Every 8th Heston case sits on an edge of the domain (V == 0, |rho| -> 1,
@@ -21,8 +22,9 @@ import pytest
 
 from paper_1901_04200_b200 import configs
 from paper_1901_04200_b200.engine import Engine
-from paper_1901_04200_b200.model import (CALL, PUT, BasketSpec, HestonParams, Instrument,
-                                         LeverageGrid, McSettings, MCConfig, ModelSpec)
+from paper_1901_04200_b200.model import (CALL, PUT, BasketSpec, BufferDrawSource, HestonParams,
+                                         Instrument, LeverageGrid, McSettings, MCConfig,
+                                         ModelSpec)
 
 from test_gpu_parity import TOL, assert_report_close, rel_err
 
@@ -101,6 +103,13 @@ def _check(ref, spec, x, opts, g, tangent_ok):
     assert_report_close(rep, orc)
     again = eng.gradient_of_G(x, targets, cfg)
     assert again.G == rep.G and again.grad == rep.grad and again.means == rep.means
+    # the same paths as caller draws (the materialised PhiloxNormalSource,
+    # antithetic pairs included, through the DRAWS kernels): the same report
+    rows = 2 * P if fresh else P
+    src = BufferDrawSource(eng.fill_normals(seed, eng.N, anti, 0, rows), eng.N)
+    viad = eng.gradient_of_G(x, targets, MCConfig(paths=P, seed=seed, fresh_step2_paths=fresh),
+                             source=src)
+    assert viad.G == rep.G and viad.grad == rep.grad and viad.means == rep.means
     if tangent_ok:
         t = eng.gradient_of_G(x, targets, cfg, method="tangent")
         assert_report_close(t, orc)
