@@ -149,8 +149,8 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
         if (DRAWS)  // caller draws: slots [k0*n, k0*n + 2*npairs) of the path's row
             copy_draws<double>(drow, valid, 2 * pair0, 2 * npairs, a.steps * n, zb);
         else
-            gen_segment<BGS>(base, neg, pair0, npairs, w.seed_lo, w.seed_hi, zb, wl, *s.tab,
-                             a.rc);
+            gen_segment<BGS, 8>(base, neg, pair0, npairs, w.seed_lo, w.seed_hi, zb, wl, *s.tab,
+                                a.rc);  // 8 central slots together (measured on config 4)
         for (uint32_t j = 0; j < nb; ++j) {
             const uint32_t k = k0 + j;
             double z[NA];
