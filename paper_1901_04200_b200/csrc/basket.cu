@@ -31,6 +31,9 @@ namespace {
 
 constexpr int NA = kMaxAssets;
 constexpr int BGS = 16;  // Philox pairs per normal batch (two steps of 16 assets)
+#ifndef LTG_BPB
+#define LTG_BPB 8  // central slots evaluated together (measured on config 4)
+#endif
 
 __device__ __forceinline__ double warp_sum_b(double v) {
 #pragma unroll
@@ -149,8 +152,8 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
         if (DRAWS)  // caller draws: slots [k0*n, k0*n + 2*npairs) of the path's row
             copy_draws<double>(drow, valid, 2 * pair0, 2 * npairs, a.steps * n, zb);
         else
-            gen_segment<BGS, 8>(base, neg, pair0, npairs, w.seed_lo, w.seed_hi, zb, wl, *s.tab,
-                                a.rc);  // 8 central slots together (measured on config 4)
+            gen_segment<BGS, LTG_BPB>(base, neg, pair0, npairs, w.seed_lo, w.seed_hi, zb, wl,
+                                      *s.tab, a.rc);
         for (uint32_t j = 0; j < nb; ++j) {
             const uint32_t k = k0 + j;
             double z[NA];
