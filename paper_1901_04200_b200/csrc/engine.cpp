@@ -490,6 +490,13 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
     a.tables = c->d_tab.as<RngTables>();
     a.rc = c->h_rc;
     a.seg_steps = c->seg_steps;
+    // plain Heston (one leverage cell equal to 1.0): the kLevUnit kernels skip
+    // the exact products by L (LTG_UNIT_LEV=0: the general kernels, tests)
+    static const bool unit_ok = [] {
+        const char* e = std::getenv("LTG_UNIT_LEV");
+        return !(e && e[0] == '0');
+    }();
+    a.unit_lev = (unit_ok && c->nlev == 1 && x[5] == 1.0) ? 1 : 0;
     a.fp32 = c->fp32;
     a.safe = c->safe;
     a.rare = c->d_counter.as<uint32_t>() + kRareSlot;

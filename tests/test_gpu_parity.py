@@ -658,3 +658,40 @@ def test_multi_rank_paths_on_one_gpu(world):
     cfg4 = MCConfig(paths=3001, seed=b4.seed)
     assert bg.gradient_of_G(b4.x, b4.targets, cfg4).to_json() == \
         Engine(b4.spec).gradient_of_G(b4.x, b4.targets, cfg4).to_json()
+
+
+_UNIT_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+from paper_1901_04200_b200 import configs
+from paper_1901_04200_b200.engine import Engine
+from paper_1901_04200_b200.model import MCConfig
+c = configs.cfg3()
+t = configs.load_targets(c)
+eng = Engine(c.spec)
+out = {}
+for prec in (0, 1):
+    for fresh in (False, True):
+        cfg = MCConfig(paths=5000, seed=c.seed, precision=prec, fresh_step2_paths=fresh)
+        out[f"{prec}{int(fresh)}"] = eng.gradient_of_G(c.x, t, cfg).to_json()
+print(json.dumps(out))
+"""
+
+
+def test_unit_leverage_kernels_bitwise_identical():
+    # configs 3/5 evaluate at L_0_0 = 1.0: the kLevUnit kernels skip the
+    # products by L (exact) — the same reports, bit for bit, as the general
+    # one-cell kernels (LTG_UNIT_LEV=0), fp64 and fp32, both pass-2 plans
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, LTG_UNIT_LEV=flag)
+        r = subprocess.run([sys.executable, "-c", _UNIT_SCRIPT, root], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        runs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert runs[0] == runs[1]
