@@ -716,20 +716,26 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     c->d_part2.ensure(table_rows * c->M * 8);
     c->d_tot2.ensure(c->M * 8);
     c->d_grad.ensure(c->M * 8);
-    HestonArgs a = heston_args(c, c->h_x.data());
+    // caller draws: pass 2 reads the rows of its own path set (the fresh
+    // step-2 rows follow the pass-1 rows in d_draws)
+    const bool fresh_rows = c->draws_on && cfg.fresh_step2_paths;
+    const double* p2_draws =
+        c->draws_on ? c->d_draws.as<double>() + (fresh_rows ? c->draws_rowsA * c->N : 0)
+                    : nullptr;
+    const uint64_t p2_row0 = fresh_rows ? c->draws_row0B : c->draws_row0A;
+    // (the Heston argument block reads x[0..5]: built for Heston contexts only)
+    HestonArgs a = c->kind == 0 ? heston_args(c, c->h_x.data()) : HestonArgs{};
     a.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
-    if (c->draws_on && cfg.fresh_step2_paths) {  // the caller rows of the fresh path set
-        a.draws = c->d_draws.as<double>() + c->draws_rowsA * c->N;
-        a.draws_row0 = c->draws_row0B;
-    }
+    a.draws = p2_draws;
+    a.draws_row0 = p2_row0;
     Work w = base_work(c, cfg, plan);
     const uint32_t nseg = (c->steps + c->seg_steps - 1) / c->seg_steps;
     cuda_check(cudaEventRecord(c->ev[3], c->stream), "event");
     if (w.n_chunks && c->kind == 1) {
         BasketArgs b = basket_args(c, c->h_x.data());
         b.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
-        b.draws = a.draws;
-        b.draws_row0 = a.draws_row0;
+        b.draws = p2_draws;
+        b.draws_row0 = p2_row0;
         b.partials = c->d_part2.as<double>() + plan.chunk_begin * c->M;
         b.use_store = have_ckpt && !cfg.fresh_step2_paths ? 1 : 0;
         b.store = b.use_store ? c->d_ckpt.as<double2>() : nullptr;
