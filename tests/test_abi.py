@@ -102,3 +102,26 @@ def test_header_is_plain_c(tmp_path):
                         "-I", os.path.join(ROOT, "include"), str(src)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_draws_entry_points_reject_missing_context_and_source():
+    # ltg_gradient_of_G_draws / ltg_estimate_means_draws validate before any
+    # device work: no context or no draw source -> LTG_EINVAL (no GPU needed)
+    import ctypes as C
+    from paper_1901_04200_b200.cabi import LTG_EINVAL, DrawsC, MCConfigC, ReportC
+    L = engine.load_library()
+    x = (C.c_double * 6)()
+    t = (C.c_double * 60)()
+    z = (C.c_double * 8)()
+    d = DrawsC(C.cast(z, C.POINTER(C.c_double)), 1, 8)
+    cfg = MCConfigC(1, 0, 0, 0, 0, 0)
+    rep = ReportC()
+    dp = C.POINTER(C.c_double)
+    assert L.ltg_gradient_of_G_draws(None, C.cast(x, dp), 6, C.cast(t, dp), 60, C.byref(d),
+                                     C.byref(cfg), C.byref(rep)) == LTG_EINVAL
+    assert L.ltg_gradient_of_G_draws(None, C.cast(x, dp), 6, C.cast(t, dp), 60, None,
+                                     C.byref(cfg), C.byref(rep)) == LTG_EINVAL
+    assert L.ltg_estimate_means_draws(None, C.cast(x, dp), 6, C.byref(d), 1, C.cast(t, dp),
+                                      None) == LTG_EINVAL
+    assert L.ltg_estimate_means_draws(None, C.cast(x, dp), 6, None, 1, C.cast(t, dp),
+                                      None) == LTG_EINVAL
