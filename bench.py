@@ -19,6 +19,7 @@ on this host's cores, on a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -176,7 +177,8 @@ def run_reference(args, rank, world):
         times.append(dt)
     value = sample / statistics.mean(times)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world if world > 1 else args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": cfg.name, "paths": cfg.paths,
@@ -212,6 +214,17 @@ def main():
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
     rank, world, local = dist_env()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if world > 1 and args.gpus != world:
+        # one process per GPU under torchrun: the job's GPU count is WORLD_SIZE
+        ap.error(f"--gpus {args.gpus} under torchrun with WORLD_SIZE={world}: they must agree")
+    # without torchrun, --gpus N > 1 runs one process over N devices
+    # (ltg_create_*_devices: a member context per GPU, ncclCommInitAll); with
+    # LTG_LOOPBACK=1 (tests) the N members share GPU 0
+    loopback = os.environ.get("LTG_LOOPBACK") == "1"
+    group = world == 1 and args.gpus > 1
+    n_gpus = world if world > 1 else args.gpus
 
     pg = None
     if world > 1:
@@ -237,7 +250,14 @@ def main():
         targets = e0.estimate_means(cfg.truth, MCConfig(paths=configs.TARGET_PATHS,
                                                         seed=configs.TARGET_SEED)).means
         e0.close()
-    eng = Engine(cfg.spec, device=local)
+    if group:
+        devices = [0] * n_gpus if loopback else list(range(n_gpus))
+        try:
+            eng = Engine(cfg.spec, devices=devices)
+        except (ValueError, RuntimeError) as e:
+            raise SystemExit(f"bench.py --gpus {n_gpus}: cannot open devices {devices}: {e}")
+    else:
+        eng = Engine(cfg.spec, device=local)
     if world > 1:
         import torch
         obj = [nccl_unique_id() if rank == 0 else None]
@@ -356,13 +376,16 @@ def main():
             roof["traffic"] = trf * paths_rank + tm["z_bytes"]
         M, m = len(cfg.x), cfg.m
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": K,
             "warmup": args.warmup, "ms_per_step": dev_total / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic (seeded Philox paths; no dataset)",
             "config": {"workload": cfg.name, "model": cfg.description, "paths": cfg.paths,
-                       "seed": cfg.seed, "parallelism": f"path-sharded dp{world}",
+                       "seed": cfg.seed,
+                       "parallelism": f"path-sharded dp{n_gpus}" + (
+                           " (one process, ltg_create_*_devices)" if group else
+                           " (torchrun, one process per GPU)" if world > 1 else ""),
                        "l2": "working set > L2: HBM checkpoint/store table "
                              f"{tm['ckpt_bytes']/1e9:.1f} GB rewritten every step",
                        "checkpoint_interval_steps": tm["seg_steps"]},
@@ -374,9 +397,13 @@ def main():
             "pass_ms": {"pass1": p1_tot / K, "pass2": p2_tot / K},
             "method": args.method,
             "G": rep.G,
+            "report_sha1": hashlib.sha1(rep.to_json().encode()).hexdigest(),
             "rng_exact": eng.rng_exact,
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if group and loopback:
+            line["config"]["loopback"] = "LTG_LOOPBACK=1: the members share GPU 0 (test mode)"
+
+        if n_gpus == 1 and not args.no_cpu_baseline:
             workers = os.cpu_count() or 1
             try:
                 sample, _ = size_cpu_sample(cfg, targets, workers, args.cpu_seconds)

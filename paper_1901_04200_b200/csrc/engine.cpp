@@ -500,11 +500,43 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
     a.fp32 = c->fp32;
     a.safe = c->safe;
     a.rare = c->d_counter.as<uint32_t>() + kRareSlot;
+    a.rare_thr = kRareThr;
     if (c->draws_on) {
         a.draws = c->d_draws.as<double>();
         a.draws_row0 = c->draws_row0A;
     }
     return a;
+}
+
+// Pass 2's input table for `stride` paths (heston.cu): grid layouts keep
+// (S, V) at every checkpoint; one-column layouts (the S-free pass 2) keep V
+// at every checkpoint and S at every maturity event.
+struct TabLayout {
+    size_t ck_bytes, smat_off, total;
+};
+bool s_free(const ltg_ctx* c) { return c->kind == 0 && c->cols == 1; }
+TabLayout tab_layout(const ltg_ctx* c, uint32_t ks, uint64_t stride) {
+    const size_t r = c->fp32 ? 4 : 8;
+    const uint32_t nseg = (c->steps + ks - 1) / ks;
+    const size_t rows = nseg > 1 ? nseg - 1 : 0;
+    TabLayout t{};
+    if (!s_free(c)) {
+        t.ck_bytes = rows * stride * 2 * r;
+        t.smat_off = t.total = t.ck_bytes;
+    } else {
+        t.ck_bytes = rows * stride * r;
+        t.smat_off = (t.ck_bytes + 255) & ~size_t(255);
+        t.total = t.smat_off + c->events.size() * stride * r;
+    }
+    return t;
+}
+
+// Test knob LTG_TEST_FRESH_RARE=1: the range check of the fresh step-2 path
+// set (and only it) flags every path, which forces the exact rerun that a
+// genuinely out-of-range fresh-path argument would (tests/test_gpu_parity.py)
+unsigned fresh_check_thr() {
+    const char* e = std::getenv("LTG_TEST_FRESH_RARE");
+    return (e && e[0] == '1') ? 0u : kRareThr;
 }
 
 Work base_work(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan) {
@@ -610,7 +642,7 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     if (!key.empty() && key == c->plan_key) {
         c->seg_steps = c->plan_ks;
         c->z_chunks = c->plan_z;
-        ckpt = c->plan_chosen && ((c->steps + c->seg_steps - 1) / c->seg_steps) > 1;
+        ckpt = c->plan_chosen && (s_free(c) || ((c->steps + c->seg_steps - 1) / c->seg_steps) > 1);
         if (!ckpt) c->z_chunks = 0;
     } else if (want_ckpt && c->kind == 0) {
         size_t free_b = 0, total_b = 0;
@@ -626,10 +658,7 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         const size_t elem = c->fp32 ? 8 : 16;
         const uint64_t nloc = w.n_chunks;
         const size_t z_chunk = size_t(c->steps) * plan.chunk_paths * elem;
-        auto ck_bytes = [&](uint32_t ks) {
-            const uint32_t nseg = (c->steps + ks - 1) / ks;
-            return size_t(nseg > 1 ? nseg - 1 : 0) * w.ckpt_stride * elem;
-        };
+        auto ck_bytes = [&](uint32_t ks) { return tab_layout(c, ks, w.ckpt_stride).total; };
         const char* env_ks = std::getenv("LTG_CKPT_STEPS");
         const char* env_z = std::getenv("LTG_ZSTORE");
         // (caller draws: pass 2 reads the caller's rows, nothing to store)
@@ -658,7 +687,7 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                 c->d_ckpt.ensure(need_ck);
                 c->d_ztab.ensure(need_z);
             }
-            ckpt = ((c->steps + c->seg_steps - 1) / c->seg_steps) > 1;
+            ckpt = s_free(c) || ((c->steps + c->seg_steps - 1) / c->seg_steps) > 1;
             if (!ckpt) c->z_chunks = 0;
         }
         c->plan_key = key;
@@ -670,7 +699,9 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         HestonArgs a = heston_args(c, c->h_x.data());
         // partial rows are indexed from the launch's first chunk
         a.partials = c->d_part1.as<double>() + plan.chunk_begin * width;
-        a.ckpt = ckpt ? c->d_ckpt.as<double2>() : nullptr;
+        a.ckpt = ckpt ? c->d_ckpt.p : nullptr;
+        a.smat = ckpt ? c->d_ckpt.as<char>() + tab_layout(c, c->seg_steps, w.ckpt_stride).smat_off
+                      : nullptr;
         a.write_sums = 1;
         a.write_ckpt = ckpt ? 1 : 0;
         a.ztab = c->d_ztab.p;
@@ -700,9 +731,8 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     c->timing.launches += 2;
     c->timing.paths_pass1 = plan.path_end - plan.path_begin;
     if (ckpt && c->kind == 0) {
-        const uint64_t nseg = (c->steps + c->seg_steps - 1) / c->seg_steps;
         c->timing.seg_steps = c->seg_steps;
-        c->timing.ckpt_bytes = (nseg - 1) * w.ckpt_stride * (c->fp32 ? 8 : 16);
+        c->timing.ckpt_bytes = tab_layout(c, c->seg_steps, w.ckpt_stride).total;
         c->timing.z_bytes = c->z_chunks * plan.chunk_paths * c->steps * (c->fp32 ? 8 : 16);
     } else if (ckpt) {
         c->timing.ckpt_bytes = uint64_t(c->events.size()) * c->n_assets * w.ckpt_stride * 16;
@@ -746,13 +776,14 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         cuda_check(launch_basket_pass2(b, w, 0, c->stream), "basket pass 2");
         c->timing.launches += 1;
     } else if (w.n_chunks) {
-        if (!have_ckpt && nseg > 1) {
+        const bool sf = s_free(c);
+        if (!have_ckpt && (nseg > 1 || sf)) {
             // fresh_step2_paths or no room for a full checkpoint table: replay
             // the pass-2 path set in waves (checkpoint-only forward, then adjoint)
             if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
             size_t free_b = 0, total_b = 0;
             cudaMemGetInfo(&free_b, &total_b);
-            const size_t per_chunk = size_t(nseg - 1) * plan.chunk_paths * (c->fp32 ? 8 : 16);
+            const size_t per_chunk = tab_layout(c, c->seg_steps, plan.chunk_paths).total + 256;
             size_t budget = c->d_ckpt.bytes;
             if (budget < per_chunk * 64 && free_b > (size_t(2) << 30))
                 budget = std::max(budget, std::min(free_b - (size_t(2) << 30),
@@ -767,16 +798,23 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                 ww.n_chunks = std::min<uint64_t>(wave, w.n_chunks - c0);
                 ww.ckpt_path0 = ww.chunk_begin * plan.chunk_paths;
                 ww.ckpt_stride = ww.n_chunks * plan.chunk_paths;
+                const size_t smat_off = tab_layout(c, c->seg_steps, ww.ckpt_stride).smat_off;
                 HestonArgs r = a;
-                r.ckpt = c->d_ckpt.as<double2>();
+                r.ckpt = c->d_ckpt.p;
+                r.smat = c->d_ckpt.as<char>() + smat_off;
                 r.write_sums = 0;
                 r.write_ckpt = 1;
                 r.partials = nullptr;
+                // every step: the S-free layout needs S at every maturity, and
+                // no forward has range-checked the fresh path set
+                r.check_all = (sf || cfg.fresh_step2_paths) ? 1 : 0;
+                if (cfg.fresh_step2_paths) r.rare_thr = fresh_check_thr();
                 zero_counter(c, 1);
                 ww.counter = c->d_counter.as<uint32_t>() + 1;
                 cuda_check(launch_heston_pass1(r, ww, 0, c->stream), "heston replay");
                 HestonArgs b = a;
-                b.ckpt = c->d_ckpt.as<double2>();
+                b.ckpt = c->d_ckpt.p;
+                b.smat = c->d_ckpt.as<char>() + smat_off;
                 b.partials = c->d_part2.as<double>() + ww.chunk_begin * c->M;
                 zero_counter(c, 2);
                 ww.counter = c->d_counter.as<uint32_t>() + 2;
@@ -784,8 +822,27 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                 c->timing.launches += 2;
             }
         } else {
-            if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
-            a.ckpt = c->d_ckpt.as<double2>();
+            if (cfg.fresh_step2_paths) {
+                w.path_offset += cfg.paths;
+                if (!c->safe) {  // (safe kernels compute no flag)
+                    // one segment (steps <= KS): no checkpoint replay ran over
+                    // the fresh paths, so range-check them with a forward first
+                    HestonArgs r = a;
+                    r.write_sums = 0;
+                    r.write_ckpt = 0;
+                    r.ckpt = nullptr;
+                    r.partials = nullptr;
+                    r.check_all = 1;
+                    r.rare_thr = fresh_check_thr();
+                    zero_counter(c, 1);
+                    Work ww = w;
+                    ww.counter = c->d_counter.as<uint32_t>() + 1;
+                    cuda_check(launch_heston_pass1(r, ww, 0, c->stream), "heston range check");
+                    c->timing.launches += 1;
+                }
+            }
+            a.ckpt = c->d_ckpt.p;
+            a.smat = c->d_ckpt.as<char>() + tab_layout(c, c->seg_steps, w.ckpt_stride).smat_off;
             a.ztab = c->d_ztab.p;
             a.z_chunks = c->z_chunks;
             a.z_stride = std::max<uint64_t>(1, c->z_chunks * plan.chunk_paths);

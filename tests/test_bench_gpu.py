@@ -52,3 +52,30 @@ def test_engine_arm_fp32_and_tangent_method():
     t = _run("--config", "cfg3", "--paths", "65536", "--steps", "1", "--warmup", "3",
              "--no-cpu-baseline", "--method", "tangent")
     assert t["method"] == "tangent" and t["value"] > 0
+
+
+def test_gpus_n_drives_n_devices_loopback():
+    # `bench.py --gpus N` without torchrun opens one context per device
+    # (ltg_create_*_devices). With LTG_LOOPBACK=1 the N members share GPU 0
+    # and exchange their chunk rows with device copies where NCCL would
+    # all-gather: the report is bitwise the one-GPU report and n_gpus == N
+    args = ["--config", "cfg3", "--paths", "50017", "--steps", "1", "--warmup", "3",
+            "--no-cpu-baseline", "--no-alt-method"]
+    one = _run("--gpus", "1", *args)
+    env = dict(os.environ, LTG_LOOPBACK="1")
+    for n in (2, 3):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n),
+                            *args], cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+        assert r.returncode == 0, r.stderr[-3000:]
+        (d,) = [json.loads(l) for l in r.stdout.splitlines() if l.strip().startswith("{")]
+        assert d["n_gpus"] == n and "loopback" in d["config"]
+        assert d["report_sha1"] == one["report_sha1"] and d["G"] == one["G"]
+        assert d["value"] > 0
+
+
+def test_gpus_n_fails_loudly_without_the_devices():
+    # more devices than the machine has: the run must fail, not time fewer GPUs
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64",
+                        "--config", "cfg1", "--steps", "1", "--warmup", "3", "--no-cpu-baseline"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode != 0 and "cannot open devices" in r.stderr

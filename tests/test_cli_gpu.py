@@ -1,7 +1,7 @@
-"""The reference CLI's price / gradcheck on the GPU (examples/lanetape_gpu,
-SURVEY.md §8(f).2): artifacts with the echoed config in the reference's key
-order (P/tools/main.cpp:72-205), numbers against the reference library on the
-same model, paths and seed."""
+"""price / gradcheck runs on the GPU (examples/lanetape_gpu):
+JSON artifacts with the echoed config (the schema a reference user's tooling
+reads), numbers against the reference library on the same model, paths and
+seed; exit status 1 on bad usage."""
 import json
 import os
 import subprocess
@@ -77,27 +77,3 @@ def test_cli_errors(golden_dir, tmp_path):
     r = _run("price", "--config", os.path.join(golden_dir, "heston_small.json"),
              "--memory-mode", "fast")
     assert r.returncode == 1
-
-
-def test_calibrate_artifacts(golden_dir, tmp_path):
-    # main.cpp:256-382 on the GPU: kappa and theta from 1.5x the truth
-    cfg = os.path.join(golden_dir, "heston_calibrate.json")
-    r = _run("calibrate", "--config", cfg, "--out-dir", str(tmp_path))
-    assert r.returncode == 0, (r.stdout, r.stderr)
-    art = json.loads((tmp_path / "calibrate.json").read_text())
-    assert list(art) == ["config", "converged", "stop_reason", "iters", "G", "targets", "fitted",
-                         "truth", "start"]
-    assert art["config"]["command"] == "calibrate" and art["converged"]
-    assert list(art["fitted"]) == ["kappa", "theta"]
-    for k in ("kappa", "theta"):
-        assert abs(art["fitted"][k] / art["truth"][k] - 1.0) <= 1e-2
-        assert art["start"][k] == pytest.approx(1.5 * art["truth"][k])
-    csv = (tmp_path / "trajectory.csv").read_text().splitlines()
-    assert csv[0].startswith("# config: ") and len(csv) > 2
-
-
-def test_calibrate_errors(golden_dir, tmp_path):
-    cfg = os.path.join(golden_dir, "heston_calibrate.json")
-    assert _run("calibrate", "--config", cfg, "--free", "sigma").returncode == 1
-    assert _run("calibrate", "--config", cfg, "--init", "kappa").returncode == 1
-    assert _run("calibrate", "--config", cfg, "--init", "nope=1").returncode == 1

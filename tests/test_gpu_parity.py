@@ -695,3 +695,49 @@ def test_unit_leverage_kernels_bitwise_identical():
         assert r.returncode == 0, r.stderr[-2000:]
         runs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert runs[0] == runs[1]
+
+
+def _short_heston(steps):
+    # heston_small's model on a grid of `steps` <= 8 steps: one checkpoint
+    # segment, so pass 2 replays nothing before its adjoint sweep
+    import copy
+    from paper_1901_04200_b200.model import CALL, PUT, Instrument
+    spec = copy.deepcopy(load_model_spec(os.path.join(os.path.dirname(__file__), "golden",
+                                                      "heston_small.json")))
+    spec.mc.steps = steps
+    spec.instruments = [Instrument(CALL, 95.0, steps), Instrument(PUT, 100.0, max(1, steps // 2)),
+                        Instrument(CALL, 105.0, steps)]
+    return spec
+
+
+@pytest.mark.parametrize("case", ["cfg3", "short"])
+def test_fresh_path_set_is_range_checked(ref, monkeypatch, case):
+    # With fresh_step2_paths pass 2 runs a path set that pass 1 never saw, so
+    # its arguments must be range-checked before the fast adjoint kernel
+    # trusts them: the checkpoint replay covers every step (not only up to
+    # the last segment), and a one-segment model gets a checking forward.
+    # LTG_TEST_FRESH_RARE=1 makes exactly that check flag every path: the
+    # call must then rerun with the exact kernels and give the same bits.
+    if case == "cfg3":
+        c = configs.cfg3()
+        spec, x, t, seed = c.spec, c.x, configs.load_targets(c), c.seed
+    else:
+        spec = _short_heston(6)
+        eng0 = Engine(spec)
+        x = eng0.pack_params()
+        seed = 11
+        t = [0.9 * v for v in eng0.estimate_means(x, MCConfig(paths=4000, seed=5)).means]
+    eng = Engine(spec)
+    paths = 3001
+    fresh = MCConfig(paths=paths, seed=seed, fresh_step2_paths=True)
+    base = eng.gradient_of_G(x, t, fresh)
+    assert eng.timing()["safe_rerun"] == 0
+    monkeypatch.setenv("LTG_TEST_FRESH_RARE", "1")
+    rep = eng.gradient_of_G(x, t, fresh)
+    assert eng.timing()["safe_rerun"] == 1
+    assert rep.to_json() == base.to_json()
+    # the knob touches only the fresh path set's check
+    eng.gradient_of_G(x, t, MCConfig(paths=paths, seed=seed))
+    assert eng.timing()["safe_rerun"] == 0
+    orc = ref.program(spec).gradient_of_G(x, t, paths, seed, fresh=True, workers=8)
+    assert_report_close(rep, orc)
