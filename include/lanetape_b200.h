@@ -21,7 +21,7 @@
  *   ltg_create_heston   <- lanetape::record_heston_program(ModelSpec) heston.hpp:327-329
  *                          (the GPU does not interpret tapes: the model description
  *                          itself is the program)
- *   ltg_pack_params     <- lanetape::pack_params                 heston.hpp:212-218
+ *   ltg_pack_params     <- lanetape::pack_params                 heston.hpp:212-219
  *
  * Conventions (mirroring expectation.hpp / tape.hpp error behaviour):
  *   return LTG_OK (0) on success;
@@ -57,7 +57,7 @@ extern "C" {
 #define LTG_ENUMERIC 2
 #define LTG_ECUDA 3
 
-/* Instrument::Kind (heston.hpp:257-263) */
+/* Instrument::Kind (heston.hpp:88-94) */
 #define LTG_CALL 0
 #define LTG_PUT 1
 
@@ -72,7 +72,7 @@ extern "C" {
 
 typedef struct ltg_ctx ltg_ctx;
 
-/* ModelSpec minus McSettings.paths/seed (heston.hpp:189-283): HestonParams,
+/* ModelSpec minus McSettings.paths/seed (heston.hpp:96-114): HestonParams,
  * LeverageGrid, instruments, steps and dt. kappa..v0 and `leverage` are the
  * values the program is "recorded" at (pack_params order); the packed
  * parameter vector x passed to the compute calls overrides them. */

@@ -2,7 +2,7 @@
 //
 // Mirrors the reference's calling surface for the ∇G path
 // (/root/reference/proj/include/lanetape/):
-//   ModelSpec / HestonParams / LeverageGrid / Instrument   heston.hpp:189-283
+//   ModelSpec / HestonParams / LeverageGrid / Instrument   heston.hpp:20-114
 //   MCConfig, GradientReport, MeansResult                  expectation.hpp:25-82
 //   gradient_of_G, estimate_means, finite_diff_gradient_of_G
 //                                                          expectation.hpp:274-400
@@ -12,7 +12,7 @@
 //
 // The reference programs against a recorded Tape; the GPU engine is built
 // from the model description the tape is recorded from
-// (record_heston_program(ModelSpec), heston.hpp:496-498), so an Engine is the
+// (record_heston_program(ModelSpec), heston.hpp:327-329), so an Engine is the
 // GPU counterpart of "record the program, freeze a Kernel".
 #pragma once
 

@@ -13,7 +13,7 @@
 
 namespace lanetape_b200 {
 
-// field-by-field copy of ModelSpec (L/heston.hpp:189-283)
+// field-by-field copy of ModelSpec (L/heston.hpp:20-114)
 inline ModelSpec to_gpu(const lanetape::ModelSpec& s) {
     ModelSpec g;
     g.heston = {s.heston.mu, s.heston.kappa, s.heston.theta, s.heston.xi,

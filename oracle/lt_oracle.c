@@ -14,7 +14,7 @@
  *   - and, bit for bit, the reference library itself compiled into
  *     oracle/_ref/libltref.so (oracle/ref_driver.cpp) on small configs.
  * The arithmetic below replays the reference's tape node order exactly
- * (forward: record_heston_program, heston.hpp:462-492; reverse:
+ * (forward: record_heston_program, heston.hpp:293-323; reverse:
  * reverse_seeded / Kernel::reverse_impl, tape.hpp:344-413,
  * kernel.hpp:212-288), so per-path outputs and adjoints are bitwise equal to
  * the reference's, and the BatchSums accumulation order
@@ -121,7 +121,7 @@ void lto_fill_normals(uint64_t seed, size_t dim, int antithetic, uint64_t path, 
 
 /* ---- heston.hpp -------------------------------------------------------- */
 
-/* floor_index, heston.hpp:242-245: largest i with nodes[i] <= x, clamped to 0 */
+/* floor_index, heston.hpp:72-76: largest i with nodes[i] <= x, clamped to 0 */
 static size_t floor_index(const double* nodes, size_t n, double x) {
     size_t cnt = 0; /* upper_bound */
     while (cnt < n && nodes[cnt] <= x) ++cnt;
@@ -132,11 +132,11 @@ size_t lto_heston_num_params(const ltg_heston_model* m) {
     return 5 + (size_t)m->n_t_nodes * m->n_s_nodes;
 }
 
-/* One path of the program record_heston_program records (heston.hpp:414-494)
+/* One path of the program record_heston_program records (heston.hpp:245-325)
  * replayed in node order, then its seeded reverse sweep (tape.hpp:344-413)
  * in reverse node order. x = [kappa, theta, xi, rho, v0, L row-major]
- * (pack_params, heston.hpp:384-388); z = 2*steps draws, slot 2k drives V and
- * slot 2k+1 the independent part of S (heston.hpp:470-471). y gets the m
+ * (pack_params, heston.hpp:212-219); z = 2*steps draws, slot 2k drives V and
+ * slot 2k+1 the independent part of S (heston.hpp:301-302). y gets the m
  * payoffs; adj (may be NULL) gets the M parameter adjoints of lambda.y.
  * Returns 2 on a domain error (sqrt of a negative; the reference throws
  * EvalError), else 0. */
@@ -146,7 +146,7 @@ int lto_heston_path(const ltg_heston_model* m, const double* x, const double* z,
     const double kappa = x[0], theta = x[1], xi = x[2], rho = x[3], v0 = x[4];
     const double* lev = x + 5;
     const double dt = m->dt, sqdt = sqrt(dt), mu_dt = m->mu * dt, half_dt = 0.5 * dt;
-    /* rho_comp = sqrt(1 - rho*rho) * sqrt(dt)  (heston.hpp:455) */
+    /* rho_comp = sqrt(1 - rho*rho) * sqrt(dt)  (heston.hpp:286) */
     const double rr = rho * rho, u = 1.0 - rr;
     if (u < 0.0) return 2;
     const double sqrtu = sqrt(u), rho_comp = sqrtu * sqdt;
@@ -163,7 +163,7 @@ int lto_heston_path(const ltg_heston_model* m, const double* x, const double* z,
         const size_t row = floor_index(m->t_nodes, m->n_t_nodes, (double)k * dt);
         size_t col = 0;
         for (size_t j = 1; j < cols; ++j)
-            if (S[k] - m->s_nodes[j] >= 0.0) col = j; /* select_ge chain, heston.hpp:466-467 */
+            if (S[k] - m->s_nodes[j] >= 0.0) col = j; /* select_ge chain, heston.hpp:297-298 */
         cell[k] = row * cols + col;
         const double L = lev[cell[k]];
         const double sqrtV = sqrt(Vp);

@@ -11,7 +11,7 @@
 //   ltref_uniform             uniform_from_bits              rng.hpp:38-40
 //   ltref_inverse_normal_cdf  inverse_normal_cdf             rng.hpp:45-85
 //   ltref_fill_normals        PhiloxNormalSource::fill       rng.hpp:113-127
-//   ltref_record_heston       record_heston_program          heston.hpp:414-494
+//   ltref_record_heston       record_heston_program          heston.hpp:245-325
 //   ltref_record_basket       a program recorded with the public Tape API
 //                             (config 4 has no model in the reference layer)
 //   ltref_gradient_of_G       gradient_of_G(Kernel, ...)     expectation.hpp:300-344
@@ -19,7 +19,7 @@
 //   ltref_forward_sums        detail::forward_pass           expectation.hpp:152-198
 //   ltref_reverse_sums        detail::reverse_pass           expectation.hpp:204-249
 //   ltref_path_adjoint        forward_eval + reverse_seeded  tape.hpp:276-413
-//   ltref_simulate_path       HestonSimulator::simulate_path heston.hpp:554-593
+//   ltref_simulate_path       HestonSimulator::simulate_path heston.hpp:385-424
 //   ltref_finite_diff_gradient_of_G                           expectation.hpp:372-400
 #include <cstdint>
 #include <cstring>

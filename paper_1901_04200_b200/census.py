@@ -16,8 +16,6 @@ tail draw, ~2% of the total) — those fractions are slightly flattering.
 """
 from __future__ import annotations
 
-from .kernels_meta import SEG_STEPS
-
 # per-path thread-level FP64 instruction counts
 PASS1_FP64 = {"cfg3_heston:fp64": 107979.0, "cfg1_gbm:fp64": 2394.0,
               "cfg2_localvol:fp64": 9945.0, "cfg4_basket16:fp64": 67307.0}
@@ -51,16 +49,6 @@ def pass2_fp64_per_path(name: str, precision: str = "fp64"):
 def dram_bytes_per_path(name: str, precision: str = "fp64", kernel: str = "pass2"):
     table = PASS1_DRAM if kernel == "pass1" else PASS2_DRAM
     return table.get(_key(name, precision))
-
-
-def ckpt_bytes(cfg) -> float:
-    """HBM checkpoint table of a 16-step interval (upper bound; the engine
-    reports the table it actually wrote in ltg_timing.ckpt_bytes)."""
-    spec = cfg.spec
-    if not hasattr(spec, "mc"):
-        return 0.0
-    nseg = (spec.mc.steps + SEG_STEPS - 1) // SEG_STEPS
-    return float(max(0, nseg - 1)) * cfg.paths * 16
 
 
 def pass1_fp32_per_path(name: str, precision: str = "fp32"):

@@ -1,7 +1,7 @@
 """The five BASELINE.json configurations expressed through the reference API.
 
 Configs 1-3 and 5 are instances of the reference's own Heston-SLV program
-(record_heston_program, heston.hpp:414-494) via the embedding of SURVEY.md
+(record_heston_program, heston.hpp:245-325) via the embedding of SURVEY.md
 §8(d): a GBM / local-vol model is Heston with kappa = xi = rho = 0,
 theta = v0 = 1 (so V == 1 exactly and sqrt(V) == 1) and the volatility carried
 by the leverage grid. Config 4 (16-asset correlated GBM) has no model in the

@@ -362,7 +362,7 @@ void init_common(ltg_ctx* c, int device) {
 }
 
 // maturity events from instrument maturity steps (stable order, like the
-// HestonSimulator bucketing, heston.hpp:524-539)
+// HestonSimulator bucketing, heston.hpp:336-375)
 void build_events(ltg_ctx* c, const std::vector<uint32_t>& mats) {
     std::vector<uint32_t> order(mats.size());
     std::iota(order.begin(), order.end(), 0u);
@@ -1068,7 +1068,7 @@ int ltg_create_heston(const ltg_heston_model* mdl, int device, ltg_ctx** out) {
     auto c = std::make_unique<ltg_ctx>();
     const int rc = guarded(c.get(), [&] {
         const ltg_heston_model& m = *mdl;
-        // validate(ModelSpec) minus McSettings.paths (heston.hpp:199-299)
+        // validate(ModelSpec) minus McSettings.paths (heston.hpp:30-130)
         require(m.s0 > 0.0, "HestonParams: s0 must be > 0");
         require(m.v0 >= 0.0, "HestonParams: v0 must be >= 0");
         require(m.theta >= 0.0, "HestonParams: theta must be >= 0");
@@ -1338,6 +1338,16 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
         check_params(ctx, x);
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
         const DrawScope draws(ctx, src, *cfg, plan);
+        // fp32 gradients are specified where the variance process stays off
+        // the truncation kink, i.e. under the Feller condition 2*kappa*theta
+        // >= xi^2 (configs 1-3/5, including the local-vol embeddings with
+        // kappa = xi = 0). Below it, V sits at max(V, 0)'s kink on many paths,
+        // where sqrt's pathwise derivative 0.5/sqrt(V) turns fp32 rounding of
+        // V into O(1) adjoint noise: refused, not approximated.
+        if (ctx->fp32 && ctx->kind == 0)
+            require(2.0 * x[0] * x[1] >= x[2] * x[2],
+                    "fp32 gradient_of_G needs the Feller condition 2*kappa*theta >= xi^2 "
+                    "(its accuracy bar is not met at the variance truncation kink); use fp64");
         const uint32_t nm = ctx->m;
         double* st = nullptr;
         // (caller draws run the exact slow paths from the start: DrawScope)

@@ -2,7 +2,7 @@
 // for bit.
 //
 // The reference draws its normals with glibc's log() (rng.hpp:61) and steps
-// S with glibc's exp() (heston.hpp:476, via tape.hpp:305 / kernel.hpp:172).
+// S with glibc's exp() (heston.hpp:307, via tape.hpp:305 / kernel.hpp:172).
 // glibc >= 2.28 implements both with the ARM optimized-routines algorithms
 // (log: x = 2^k z, 128-entry (1/c, log c) table, degree-5 polynomial in
 // r = z/c - 1; exp: x = k ln2/128 + r, 128-entry 2^(j/128) table, degree-5

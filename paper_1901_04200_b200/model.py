@@ -1,9 +1,9 @@
 """Model and configuration types, mirroring the reference's model layer.
 
 Python mirror of ``lanetape``'s ``HestonParams``/``LeverageGrid``/``Instrument``/
-``McSettings``/``ModelSpec`` (heston.hpp:189-283), their validation
-(heston.hpp:199-299), JSON I/O with the reference's key layout
-(heston.hpp:301-379) and ``pack_params``/``unpack_params`` (heston.hpp:381-401);
+``McSettings``/``ModelSpec`` (heston.hpp:20-114), their validation
+(heston.hpp:30-130), JSON I/O with the reference's key layout
+(heston.hpp:132-210) and ``pack_params``/``unpack_params`` (heston.hpp:212-232);
 plus ``MCConfig``/``GradientReport``/``MeansResult`` (expectation.hpp:25-82).
 These are plain host-side descriptions: the CUDA engine receives them through
 the C ABI in ``include/lanetape_b200.h``.
@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
 CALL, PUT = 0, 1
-HESTON_FREE_PARAMS = 5  # heston.hpp:382
+HESTON_FREE_PARAMS = 5  # heston.hpp:213
 
 
 @dataclass
@@ -32,7 +32,7 @@ class HestonParams:
 
 
 def validate_params(p: HestonParams) -> None:
-    """heston.hpp:199-210"""
+    """heston.hpp:30-41"""
     def bad(what):
         raise ValueError("HestonParams: " + what)
     if not (p.s0 > 0.0):
@@ -68,7 +68,7 @@ class LeverageGrid:
 
 
 def validate_grid(g: LeverageGrid) -> None:
-    """heston.hpp:226-239"""
+    """heston.hpp:57-70"""
     def bad(what):
         raise ValueError("LeverageGrid: " + what)
     if not g.t_nodes or not g.s_nodes:
@@ -87,7 +87,7 @@ def validate_grid(g: LeverageGrid) -> None:
 
 
 def floor_index(nodes: Sequence[float], x: float) -> int:
-    """heston.hpp:242-245: largest i with nodes[i] <= x, clamped to 0."""
+    """heston.hpp:72-76: largest i with nodes[i] <= x, clamped to 0."""
     i = bisect.bisect_right(list(nodes), x)
     return 0 if i == 0 else i - 1
 
@@ -116,7 +116,7 @@ class ModelSpec:
 
 
 def validate_spec(s: ModelSpec, check_paths: bool = True) -> None:
-    """heston.hpp:272-299"""
+    """heston.hpp:116-130"""
     validate_params(s.heston)
     validate_grid(s.grid)
     if check_paths and s.mc.paths == 0:
@@ -135,7 +135,7 @@ def validate_spec(s: ModelSpec, check_paths: bool = True) -> None:
 
 
 def model_spec_from_json(j: dict) -> ModelSpec:
-    """heston.hpp:301-344 (same keys; rows of grid.values are t-major)."""
+    """heston.hpp:132-175 (same keys; rows of grid.values are t-major)."""
     h = j["heston"]
     s = ModelSpec()
     s.heston = HestonParams(mu=float(h["mu"]), kappa=float(h["kappa"]), theta=float(h["theta"]),
@@ -161,7 +161,7 @@ def model_spec_from_json(j: dict) -> ModelSpec:
 
 
 def to_json(s: ModelSpec) -> dict:
-    """heston.hpp:346-371 (key order pinned)."""
+    """heston.hpp:177-202 (key order pinned)."""
     cols = s.grid.cols()
     return {
         "heston": {"kappa": s.heston.kappa, "theta": s.heston.theta, "xi": s.heston.xi,
@@ -176,18 +176,18 @@ def to_json(s: ModelSpec) -> dict:
 
 
 def load_model_spec(path: str) -> ModelSpec:
-    """heston.hpp:373-379"""
+    """heston.hpp:204-210"""
     with open(path) as f:
         return model_spec_from_json(json.load(f))
 
 
 def pack_params(p: HestonParams, g: LeverageGrid) -> List[float]:
-    """heston.hpp:384-388: [kappa, theta, xi, rho, v0, L row-major]."""
+    """heston.hpp:212-219: [kappa, theta, xi, rho, v0, L row-major]."""
     return [p.kappa, p.theta, p.xi, p.rho, p.v0] + list(g.values)
 
 
 def unpack_params(x: Sequence[float], p: HestonParams, g: LeverageGrid) -> None:
-    """heston.hpp:392-401"""
+    """heston.hpp:221-232"""
     if len(x) != HESTON_FREE_PARAMS + len(g.values):
         raise ValueError("unpack_params: packed size mismatch")
     p.kappa, p.theta, p.xi, p.rho, p.v0 = (float(v) for v in x[:5])

@@ -65,7 +65,7 @@ def test_shard_plan_rejects_bad_arguments():
 
 
 def test_model_validation_precedes_device_use(golden_dir):
-    # std::invalid_argument sites of heston.hpp:199-299 -> LTG_EINVAL (ValueError)
+    # std::invalid_argument sites of heston.hpp:30-130 -> LTG_EINVAL (ValueError)
     spec = load_model_spec(os.path.join(golden_dir, "heston_small.json"))
     spec.instruments[0].maturity_step = spec.mc.steps + 1
     with pytest.raises(ValueError, match="maturity_step"):

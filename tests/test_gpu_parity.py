@@ -206,40 +206,53 @@ def test_basket_multi_maturity_puts(ref):
         assert_report_close(rep, orc)
 
 
-# fp32 mode vs the fp64 oracle on the same paths. The bar is
-# stated for the config it is specified for (config 5 = config 3's model,
-# Feller condition 2*kappa*theta > xi^2 holds). heston_small (dt = 1/16,
-# 2*kappa*theta < xi^2) puts V at the truncation kink on most paths, where the
-# pathwise derivative of sqrt(V) is 0.5/sqrt(V): a V of 1e-12 in fp64 is noise
-# in fp32, so single paths decide the kappa/theta/xi adjoints. Measured fp32 vs
-# fp64 over seeds 3-5 and 2^12..2^20 paths: 1e-4 to 0.25, not shrinking with
-# the path count (heavy tails, not averaging noise) — the grad bar there is a
-# sanity bound; means and G keep the config-5 bars.
-FP32_TOL = {"cfg3": {"means": 1e-4, "G": 1e-3, "grad": 1e-3},
-            "heston_small": {"means": 1e-4, "G": 1e-3, "grad": 0.5}}
+# fp32 mode vs the fp64 oracle on the same paths, one bar per
+# BASELINE config the mode accepts (measured errors in the comments: at the
+# sizes below, gpurun_out/fp32_error.log). Relative errors use the floors
+# 1e-6 * max|means| and 1e-3 * max|grad|. Config 2's bar is the widest: its 40
+# leverage cells include outer spot buckets that few paths visit, and an fp32
+# path that lands on the other side of a bucket boundary moves that step's
+# leverage adjoint to the neighbouring cell.
+FP32_TOL = {"cfg1": {"means": 1e-5, "G": 1e-4, "grad": 1e-4},     # 7.5e-7 / 9.0e-6 / 1.5e-5
+            "cfg2": {"means": 1e-5, "G": 1e-4, "grad": 5e-3},     # 3.3e-6 / 9.2e-6 / 1.8e-3
+            "cfg3": {"means": 1e-4, "G": 1e-3, "grad": 1e-3}}     # 2.0e-5 / 1.2e-4 / 9.8e-5
 
 
-@pytest.mark.parametrize("name,paths", [("cfg3", 1 << 14), ("heston_small", 4096)])
-def test_fp32_mode_against_fp64_oracle(ref, golden_dir, name, paths):
-    # config 5's fp32 variant: float state/adjoint, float AS241 on the same
-    # Philox words; grad relative error with a floor of 1e-3 * max|grad|
+@pytest.mark.parametrize("name,paths", [("cfg1", 1 << 16), ("cfg2", 1 << 14), ("cfg3", 1 << 14),
+                                        ("cfg2", 1 << 20), ("cfg3", 1 << 20)])
+def test_fp32_mode_against_fp64_oracle(ref, name, paths):
+    # float state/adjoint and float AS241 on the same Philox words
     from paper_1901_04200_b200.model import FP32
     tol = FP32_TOL[name]
-    if name == "heston_small":
-        spec = load_model_spec(f"{golden_dir}/heston_small.json")
-        prog = ref.program(spec)
-        x = prog.initial_params()
-        t = 0.9 * prog.estimate_means(x, paths, 3, workers=8)[0]
-        seed = 3
-    else:
-        c = configs.ALL[name]()
-        spec, x, t, seed = c.spec, c.x, configs.load_targets(c), c.seed
-        prog = ref.program(spec)
-    orc = prog.gradient_of_G(x, t, paths, seed, workers=8)
-    rep = Engine(spec).gradient_of_G(x, t, MCConfig(paths=paths, seed=seed, precision=FP32))
+    c = configs.ALL[name]()
+    t = configs.load_targets(c) or c.targets
+    prog = ref.program(c.spec)
+    orc = prog.gradient_of_G(c.x, t, paths, c.seed, workers=os.cpu_count())
+    rep = Engine(c.spec).gradient_of_G(c.x, t, MCConfig(paths=paths, seed=c.seed, precision=FP32))
     assert rel_err(rep.means, orc["means"], 1e-6) <= tol["means"]
     assert rel_err([rep.G], [orc["G"]]) <= tol["G"]
     assert rel_err(rep.grad, orc["grad"], 1e-3) <= tol["grad"]
+
+
+def test_fp32_gradient_refused_below_feller(ref, golden_dir):
+    # heston_small (2*kappa*theta = 0.12 < xi^2 = 0.25): V sits at the
+    # truncation kink on many paths and fp32 adjoints are off by up to 0.25
+    # (measured over seeds 3-5, 2^12..2^20 paths) — the gradient is refused;
+    # fp32 means still meet their bar
+    from paper_1901_04200_b200.model import FP32
+    spec = load_model_spec(f"{golden_dir}/heston_small.json")
+    prog = ref.program(spec)
+    x = prog.initial_params()
+    eng = Engine(spec)
+    with pytest.raises(ValueError, match="Feller"):
+        eng.gradient_of_G(x, [1.0] * eng.m, MCConfig(paths=4096, seed=3, precision=FP32))
+    means, _ = prog.estimate_means(x, 4096, 3, workers=8)
+    r = eng.estimate_means(x, MCConfig(paths=4096, seed=3, precision=FP32))
+    assert rel_err(r.means, means, 1e-6) <= 1e-4
+    # at the Feller boundary itself the call is accepted
+    xb = list(x)
+    xb[2] = (2.0 * x[0] * x[1]) ** 0.5
+    eng.gradient_of_G(xb, [1.0] * eng.m, MCConfig(paths=1024, seed=3, precision=FP32))
 
 
 def test_estimate_means_and_std_errors(ref, small):

@@ -57,7 +57,10 @@ def main():
         eng.gradient_of_G(x, t, MCConfig(paths=paths + 7, seed=4))
         os.environ.pop("LTG_ZSTORE")
         eng.gradient_of_G(x, t, MCConfig(paths=paths, seed=5, fresh_step2_paths=True))
-        eng.gradient_of_G(x, t, MCConfig(paths=paths, seed=5, precision=FP32))
+        try:  # (fp32 gradients need the Feller condition)
+            eng.gradient_of_G(x, t, MCConfig(paths=paths, seed=5, precision=FP32))
+        except ValueError:
+            pass
         eng.estimate_means(x, MCConfig(paths=paths, seed=6))
         try:
             eng.gradient_of_G(x, t, MCConfig(paths=paths, seed=7), method="tangent")
