@@ -28,8 +28,13 @@
  *   LTG_EINVAL (1)   where the reference throws std::invalid_argument
  *                    (size mismatches, paths == 0, bad model, fresh_step2_paths
  *                    with store mode, ...);
- *   LTG_ENUMERIC (2) where the reference throws EvalError (a non-finite
- *                    result — the CLI maps this to exit code 2);
+ *   LTG_ENUMERIC (2) where the reference throws EvalError: the recorded
+ *                    Heston program's sqrt(1 - rho^2) of a negative value
+ *                    (heston.hpp:286, tape.hpp:261-263). Non-finite parameters
+ *                    and non-finite results are NOT errors, as in the reference
+ *                    library: the report carries the NaN / inf values (the
+ *                    reference CLI's require_finite, tools/main.cpp, is the
+ *                    caller's business; examples/lanetape_gpu exits 2 on them);
  *   LTG_ECUDA (3)    CUDA / NCCL runtime failure (no reference analogue);
  *   ltg_last_error(ctx) returns the message of the last failure on that
  *   context (ctx == NULL: last failure of a create call on this thread).
@@ -113,9 +118,18 @@ typedef struct ltg_basket_model {
 } ltg_basket_model;
 
 /* MCConfig (expectation.hpp:25-39). lane_width / worker_threads /
- * store_limit_bytes are CPU execution knobs with no GPU meaning; they are
- * accepted and ignored, as the reference's results do not depend on them
- * beyond summation order. */
+ * store_limit_bytes are CPU execution knobs with no GPU meaning and have no
+ * field here (the C++ mirror, lanetape_b200.hpp, accepts and ignores them).
+ * In particular the reference's store-mode budget check (expectation.hpp:
+ * 307-319: std::invalid_argument when nodes x lanes x batches doubles exceed
+ * store_limit_bytes) is NOT applied: memory_mode is echoed into the report
+ * and the engine keeps its own device-memory plan (HBM checkpoints, the draw
+ * store), which is bounded instead by ltg_set_hbm_budget. The reference's
+ * other store-mode check, store + fresh_step2_paths -> invalid, is kept.
+ * precision = LTG_FP32 (config 5's variant): Heston-SLV programs only;
+ * gradients additionally need the Feller condition 2*kappa*theta >= xi^2 of
+ * the parameters passed (LTG_EINVAL otherwise; DESIGN.md §6 states the
+ * per-config accuracy bars). */
 typedef struct ltg_mc_config {
     uint64_t paths;
     uint64_t seed;

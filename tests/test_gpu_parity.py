@@ -494,6 +494,31 @@ def test_error_behaviour(small):
         eng.gradient_of_G(bad, [1.0] * 4, MCConfig(paths=10, seed=1))
 
 
+@pytest.mark.parametrize("j,val", [(0, float("nan")), (4, float("inf")), (2, 1e300)])
+def test_nonfinite_values_propagate_like_the_reference(ref, j, val):
+    # the reference library's gradient_of_G returns NaN / inf instead of
+    # throwing (only a negative sqrt argument is an EvalError); so does the
+    # engine: LTG_OK with the same non-finite pattern in means and G, and
+    # the finite entries within the usual bar
+    c = configs.cfg3()
+    prog = ref.program(c.spec)
+    t = configs.load_targets(c)
+    x = list(c.x)
+    x[j] = val
+    orc = prog.gradient_of_G(x, t, 2000, c.seed, workers=8)
+    rep = Engine(c.spec).gradient_of_G(x, t, MCConfig(paths=2000, seed=c.seed))
+    pairs = [(rep.means, orc["means"]), ([rep.G], [orc["G"]])]
+    if np.all(np.isfinite(orc["grad"])):
+        pairs.append((rep.grad, orc["grad"]))
+    for a, b in pairs:
+        a, b = np.asarray(a, float), np.asarray(b, float)
+        assert np.array_equal(np.isnan(a), np.isnan(b)), (a, b)
+        assert np.array_equal(np.isinf(a), np.isinf(b)), (a, b)
+        f = np.isfinite(a)
+        if f.any():
+            assert rel_err(a[f], b[f]) <= TOL
+
+
 # ------------------------------------- per-chunk parity at full P (§8c) ----
 
 def _chunk_lambda(m):
