@@ -27,6 +27,8 @@ import subprocess
 import sys
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -267,8 +269,15 @@ def main():
                   precision=FP32 if args.precision == "fp32" else FP64)
 
     clk = Clocks(local).start()
+    # the C-ABI call on host buffers (the adjoint; the tangent method through
+    # the Python wrapper), as a C / C++ caller of ltg_gradient_of_G makes it
+    if args.method == "adjoint":
+        call, xbuf, tbuf, _ = eng.prepared_gradient(cfg.x, targets, mc)
+        x_host = np.asarray(cfg.x, dtype=np.float64)
     for _ in range(args.warmup):
         eng.gradient_of_G(cfg.x, targets, mc, method=args.method)
+        if args.method == "adjoint":
+            call()
 
     # ---- timed region: K full gradient_of_G calls ----
     if pg:
@@ -277,9 +286,14 @@ def main():
     e0 = time.time()
     wall = 0.0
     for _ in range(args.steps):
-        # host buffers in, report out, synced: the public call, wall-timed
+        # host buffers in (x copied into the caller's array), report out,
+        # synchronised: the public C-ABI call, wall-timed
         t0 = time.perf_counter()
-        rep = eng.gradient_of_G(cfg.x, targets, mc, method=args.method)
+        if args.method == "adjoint":
+            np.copyto(xbuf, x_host)
+            call()
+        else:
+            eng.gradient_of_G(cfg.x, targets, mc, method=args.method)
         wall += time.perf_counter() - t0
         tm = eng.timing()  # the call's device events (outside the e2e clock)
         dev_ms.append(tm["total_ms"])
@@ -288,6 +302,7 @@ def main():
         launches += tm["launches"]
     clk.mark(e0, time.time())
     clk.stop()
+    rep = eng.gradient_of_G(cfg.x, targets, mc, method=args.method)  # (the report, untimed)
     clocks = clk.summary()
     dev_total = sum(dev_ms)
     if pg:
@@ -340,40 +355,58 @@ def main():
         fp32 = args.precision == "fp32"
         # fp64: FP64 issue; fp32 mode: its FP32 arithmetic against the FFMA rate
         peak = probe_fp32_rate(local) if fp32 else probe_fp64_rate(local)
-        # dominant kernel of the step (device time), its frozen census
+        # dominant kernel of the step (device time) and the census of both
+        # passes (census.py): ALGORITHMIC = the kernels' executed floating-point
+        # instructions minus their redundant ones (AS241's central branch on
+        # tail slots); pass 2 weighted by the share of paths whose draws came
+        # from the draw store (z_bytes) instead of being regenerated
         dom = "pass2" if p2_tot >= p1_tot else "pass1"
         basket = not hasattr(cfg.spec, "mc")
         kname = ("basket_" if basket else "heston_") + dom + "_kernel"
-        if fp32:
-            w1, w2 = census.pass1_fp32_per_path, census.pass2_fp32_per_path
-        else:
-            w1, w2 = census.pass1_fp64_per_path, census.pass2_fp64_per_path
-        w = (w2 if dom == "pass2" else w1)(cfg.name, args.precision)
-        if args.method == "tangent":  # one forward+tangent kernel; no frozen census
-            kname, w = "heston_tangent_kernel", None
+        prec = args.precision
+        steps = cfg.spec.steps if basket else cfg.spec.mc.steps
+        elem = 8 if fp32 else 16
         paths_rank = tm["paths_pass2"] if dom == "pass2" else tm["paths_pass1"]
+        zf = 0.0 if basket else min(1.0, tm["z_bytes"] / (steps * elem * max(1, tm["paths_pass1"])))
+        w = {b: {k: census.per_path(cfg.name, prec, k, zf, b) for k in ("pass1", "pass2")}
+             for b in ("algorithmic", "executed")}
+        if args.method == "tangent":  # one forward+tangent kernel; no census
+            kname = "heston_tangent_kernel"
+            w = {b: {"pass1": None, "pass2": None} for b in w}
         t_dom = (p2_tot if dom == "pass2" else p1_tot) / K * 1e-3
-        achieved = (w * paths_rank / t_dom) if w else None
-        w_all = [w1(cfg.name, args.precision), w2(cfg.name, args.precision)]
-        if args.method == "tangent":
-            w_all = [None]
+        t_step = dev_total / K * 1e-3
+
+        def rate(basis, kernels, t):
+            ws = [w[basis][k] for k in kernels]
+            return sum(ws) * paths_rank / t if all(v is not None for v in ws) else None
+
+        achieved = rate("algorithmic", [dom], t_dom)
+        ach_exec = rate("executed", [dom], t_dom)
+        step_alg = rate("algorithmic", ["pass1", "pass2"], t_step)
+        step_exec = rate("executed", ["pass1", "pass2"], t_step)
         roof = {"bound": "fp32" if fp32 else "fp64", "kernel": kname,
                 "achieved": achieved / 1e12 if achieved else None,
                 "peak": peak / 1e12, "unit": "T fp32-inst/s" if fp32 else "T fp64-inst/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
-                "census_inst_per_path": w,
-                "whole_step_frac": (sum(w_all) * cfg.paths * K / (dev_total * 1e-3) / peak)
-                if all(w_all) else None,
+                "basis": ("algorithmic: the kernels' executed " +
+                          ("FADD+FMUL+FFMA" if fp32 else "DADD+DMUL+DFMA") +
+                          " per path (ncu census, profiles/r2_census.txt) minus the redundant "
+                          "AS241 central-branch evaluations on tail slots; pass 2 weighted by "
+                          "the draw-store share"),
+                "census_inst_per_path": {b: w[b] for b in w},
+                "draw_store_path_fraction": zf,
+                "executed_frac": (ach_exec / peak) if ach_exec else None,
+                "whole_step_frac": (step_alg / peak) if step_alg else None,
+                "whole_step_executed_frac": (step_exec / peak) if step_exec else None,
                 "peak_source": ("measured in this run: ltg_probe_fp32_rate (FFMA streams; 8 "
                                 "chains/thread, full occupancy)") if fp32 else
                                ("measured in this run: ltg_probe_fp64_rate (fastest of DFMA, "
                                 "DMUL+DADD, DADD streams; 8 chains/thread, full occupancy)")}
-        trf = census.dram_bytes_per_path(cfg.name, args.precision, dom)
+        trf = census.dram_per_path(cfg.name, prec, dom, zf)
         if trf is not None and args.method == "adjoint":
-            # ncu bytes/path without the draw store (checkpoint table), plus
-            # the draw store this call wrote (pass 1) and read back (pass 2):
-            # pass 2 with draws measures 1,527 + 756*16 B/path (profiles/r1_v12_cfg3_full.txt)
-            roof["traffic"] = trf * paths_rank + tm["z_bytes"]
+            # ncu DRAM bytes/path of the dominant kernel (with and without the
+            # draw store), weighted like the census; per launch
+            roof["traffic"] = trf * paths_rank
         M, m = len(cfg.x), cfg.m
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": K,

@@ -167,7 +167,9 @@ typedef struct ltg_timing {
     uint64_t z_bytes;            /* HBM draw store written by pass 1 (read by pass 2) */
     uint32_t safe_rerun;         /* 1: a fast kernel flagged an out-of-range argument and
                                     the call was redone with the exact slow paths */
-    uint32_t reserved;
+    uint32_t graph;              /* 0: the call's work was enqueued eagerly; 1: captured into
+                                    a CUDA graph (second call of its shape); 2: replayed from
+                                    that graph (single-GPU contexts; LTG_GRAPH=0 disables) */
 } ltg_timing;
 
 /* Path sharding plan: the path set is cut into fixed chunks whose size

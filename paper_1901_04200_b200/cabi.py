@@ -74,7 +74,7 @@ class TimingC(C.Structure):
         ("pass1_ms", C.c_double), ("pass2_ms", C.c_double), ("reduce_ms", C.c_double),
         ("total_ms", C.c_double), ("paths_pass1", C.c_uint64), ("paths_pass2", C.c_uint64),
         ("launches", C.c_uint32), ("seg_steps", C.c_uint32), ("ckpt_bytes", C.c_uint64),
-        ("z_bytes", C.c_uint64), ("safe_rerun", C.c_uint32), ("reserved", C.c_uint32),
+        ("z_bytes", C.c_uint64), ("safe_rerun", C.c_uint32), ("graph", C.c_uint32),
     ]
 
 

@@ -1,59 +1,116 @@
-"""Frozen FP64 work census of the ∇G kernels (the roofline numerator).
+"""Work census of the ∇G pass kernels: the roofline numerator of bench.py.
 
-W = FP64 instructions per path that the algorithm executes for useful lanes:
-thread-level DADD + DMUL + DFMA with predicate on, counted by ncu
-(smsp__sass_thread_inst_executed_op_{dadd,dmul,dfma}_pred_on.sum) on one
-launch and divided by the launch's path count. Lanes idled by divergence
-are NOT counted, so achieved/peak is the useful fraction of the FP64 pipe.
-Numbers are frozen per (config, precision, kernel) in DESIGN.md §5 and only
-change when the algorithm changes (not when it is tuned).
+EXECUTED — what the current kernels execute per path, counted by ncu
+(thread-level DADD + DMUL + DFMA with predicate on; the fp32 mode: FADD +
+FMUL + FFMA), one launch divided by its path count. Pass 2 has two rows:
+"regen" (the chunk's draws are regenerated from Philox) and "store" (pass 1
+kept them in the HBM draw store and pass 2 reads them); a call's pass-2
+figure is the two weighted by the fraction of its paths whose draws were
+stored (bench.py reads that from ltg_timing.z_bytes).
+Source: profiles/r2_census.txt (cfg3 at 2^20, cfg1 at 2^16, cfg2 and cfg4 at
+2^18 paths; the r2 kernels: S-free pass 2, V-only checkpoints).
 
-cfg3/cfg5 are frozen from the first implementation (profiles/r1_v1_cfg3_full.txt),
-which evaluated exactly one AS241 branch per draw. cfg1/cfg2/cfg4 were first
-counted on the v4 kernels (profiles/r1_v4_census.txt), which evaluate the
-central branch on every draw (about 6 FP64 instructions of redundant work per
-tail draw, ~2% of the total) — those fractions are slightly flattering.
+ALGORITHMIC — EXECUTED minus the kernels' only redundant floating-point work:
+gen_segment evaluates AS241's central branch for every slot of a batch,
+branch-free, and overwrites the tail slots (|q| > 0.425, probability exactly
+0.15) in a warp-compacted second phase; the central evaluation of a tail slot
+is wasted (CENTRAL_OPS instructions), and so is that of the padding slots of a
+batch shorter than the central batch width. Everything else the kernels
+execute is work of the algorithm they implement (the hand-derived adjoint;
+pass 2 replays V only, so S's exp is neither executed nor credited).
 """
 from __future__ import annotations
 
-# per-path thread-level FP64 instruction counts
-PASS1_FP64 = {"cfg3_heston:fp64": 107979.0, "cfg1_gbm:fp64": 2394.0,
-              "cfg2_localvol:fp64": 9945.0, "cfg4_basket16:fp64": 67307.0}
-PASS2_FP64 = {"cfg3_heston:fp64": 143004.0, "cfg1_gbm:fp64": 2960.0,
-              "cfg2_localvol:fp64": 12346.0, "cfg4_basket16:fp64": 503.0}
-# fp32 mode: thread-level FADD + FFMA + FMUL per path (the arithmetic the FP32
-# pipe executes), counted without the draw store on the r1 kernels (cfg3 fp32
-# at 2^18, LTG_ZSTORE=0); the mode also keeps ~6-7k FP64 instructions per pass
-# (the exact uniform and tail arguments) and all of Philox
-PASS1_FP32 = {"cfg3_heston:fp32": 45249.3}
-PASS2_FP32 = {"cfg3_heston:fp32": 67958.8}
-# per-path DRAM bytes (ncu dram__bytes_read+write / paths), latest capture without the
-# draw store (profiles/r1_v12_cfg3_noz_full.txt: the regime of cfg5 on one GPU)
-PASS1_DRAM = {"cfg3_heston:fp64": 1455.8}
-PASS2_DRAM = {"cfg3_heston:fp64": 1526.4}
+from typing import Dict, Optional, Tuple
+
+# AS241 central branch per slot (rng.cuh gen_segment phase B): r = c - q*q
+# (2), two degree-7 Horner chains with separate multiply and add (28), q*num
+# (1), the correctly rounded division (8 DFMA/DMUL around MUFU.RCP64H) = 39.
+# fp32 mode: FFMA for r, 14 FFMA, FMUL q*num, FMUL by the MUFU reciprocal = 17.
+CENTRAL_OPS = {"fp64": 39.0, "fp32": 17.0}
+TAIL_FRACTION = 0.15  # P(|p - 0.5| > 0.425), p uniform
+
+# name -> (steps, draws per path)
+SHAPE = {"cfg1_gbm": (16, 32), "cfg2_localvol": (64, 128), "cfg3_heston": (756, 1512),
+         "cfg4_basket16": (50, 800)}
+
+# (config, precision) -> {kernel: executed instructions per path}
+EXECUTED: Dict[Tuple[str, str], Dict[str, float]] = {
+    ("cfg3_heston", "fp64"): {"pass1": 102722.9, "pass2_regen": 106047.7, "pass2_store": 30466.4},
+    ("cfg3_heston", "fp32"): {"pass1": 39733.9, "pass2_regen": 53372.4, "pass2_store": 23586.5},
+    ("cfg1_gbm", "fp64"): {"pass1": 2310.0, "pass2_regen": 2406.8, "pass2_store": 814.1},
+    ("cfg1_gbm", "fp32"): {"pass1": 902.3, "pass2_regen": 1227.4, "pass2_store": 597.1},
+    ("cfg2_localvol", "fp64"): {"pass1": 9345.7, "pass2_regen": 11267.9, "pass2_store": 5036.9},
+    ("cfg2_localvol", "fp32"): {"pass1": 3625.4, "pass2_regen": 5438.4, "pass2_store": 2917.1},
+    # the basket's pass 2 is a store-mode epilogue (no draws, no replay)
+    ("cfg4_basket16", "fp64"): {"pass1": 65763.8, "pass2_regen": 455.1, "pass2_store": 455.1},
+}
+
+# DRAM bytes per path (ncu dram__bytes_read + write), without / with the draw store
+DRAM: Dict[Tuple[str, str], Dict[str, float]] = {
+    ("cfg3_heston", "fp64"): {"pass1": 753.2, "pass1_store": 12848.5, "pass2_regen": 807.9,
+                              "pass2_store": 12908.6},
+    ("cfg3_heston", "fp32"): {"pass1": 351.1, "pass1_store": 6401.7, "pass2_regen": 405.4,
+                              "pass2_store": 6453.1},
+}
+
+# central-batch widths and normal batches of the kernels (heston.cu: kPass1PB,
+# kPass2PB, kGenSteps; the checkpoint interval KS = 8 of every BASELINE plan)
+_PB = {("fp64", "pass1"): 8, ("fp32", "pass1"): 4, ("fp64", "pass2"): 16, ("fp32", "pass2"): 8}
+_BATCH_STEPS = 8
 
 
-def _key(name: str, precision: str):
-    base = "cfg3_heston" if name.startswith("cfg5") else name
-    return f"{base}:{precision}"
+def _key(name: str, precision: str) -> Tuple[str, str]:
+    return ("cfg3_heston" if name.startswith("cfg5") else name, precision)
 
 
-def pass1_fp64_per_path(name: str, precision: str = "fp64"):
-    return PASS1_FP64.get(_key(name, precision))
+def _pad_slots(steps: int, pb: int) -> int:
+    """central evaluations of slots past a short batch's end, per path"""
+    pad = 0
+    for k0 in range(0, steps, _BATCH_STEPS):
+        ns = 2 * min(_BATCH_STEPS, steps - k0)
+        pad += -(-ns // pb) * pb - ns
+    return pad
 
 
-def pass2_fp64_per_path(name: str, precision: str = "fp64"):
-    return PASS2_FP64.get(_key(name, precision))
+def redundant(name: str, precision: str, kernel: str) -> float:
+    """wasted central-branch instructions per path of one launch"""
+    base, _ = _key(name, precision)
+    if base not in SHAPE or kernel == "pass2_store":
+        return 0.0
+    if base == "cfg4_basket16":  # one RNG pass (pass 1); the epilogue draws nothing
+        return CENTRAL_OPS[precision] * TAIL_FRACTION * SHAPE[base][1] if kernel == "pass1" else 0.0
+    steps, draws = SHAPE[base]
+    pad = _pad_slots(steps, _PB[(precision, kernel[:5])])
+    return CENTRAL_OPS[precision] * (TAIL_FRACTION * draws + pad)
 
 
-def dram_bytes_per_path(name: str, precision: str = "fp64", kernel: str = "pass2"):
-    table = PASS1_DRAM if kernel == "pass1" else PASS2_DRAM
-    return table.get(_key(name, precision))
+def executed(name: str, precision: str, kernel: str) -> Optional[float]:
+    return EXECUTED.get(_key(name, precision), {}).get(kernel)
 
 
-def pass1_fp32_per_path(name: str, precision: str = "fp32"):
-    return PASS1_FP32.get(_key(name, precision))
+def algorithmic(name: str, precision: str, kernel: str) -> Optional[float]:
+    e = executed(name, precision, kernel)
+    return None if e is None else e - redundant(name, precision, kernel)
 
 
-def pass2_fp32_per_path(name: str, precision: str = "fp32"):
-    return PASS2_FP32.get(_key(name, precision))
+def per_path(name: str, precision: str, kernel: str, store_fraction: float = 0.0,
+             basis: str = "algorithmic") -> Optional[float]:
+    """census of `kernel` ("pass1" or "pass2") for a call in which
+    `store_fraction` of the paths had their draws in the draw store"""
+    f = algorithmic if basis == "algorithmic" else executed
+    if kernel == "pass1":
+        return f(name, precision, "pass1")
+    a, b = f(name, precision, "pass2_regen"), f(name, precision, "pass2_store")
+    if a is None or b is None:
+        return None
+    return (1.0 - store_fraction) * a + store_fraction * b
+
+
+def dram_per_path(name: str, precision: str, kernel: str, store_fraction: float = 0.0):
+    t = DRAM.get(_key(name, precision))
+    if t is None:
+        return None
+    if kernel == "pass1":
+        return (1.0 - store_fraction) * t["pass1"] + store_fraction * t["pass1_store"]
+    return (1.0 - store_fraction) * t["pass2_regen"] + store_fraction * t["pass2_store"]

@@ -328,8 +328,7 @@ cudaError_t blaunch(K kernel, const BasketArgs& a, const Work& w, int grid, size
     if (grid <= 0) grid = resident;
     if ((uint64_t)grid > w.n_chunks) grid = (int)w.n_chunks;
     if (grid < 1) grid = 1;
-    kernel<<<grid, kBlock, smem, st>>>(a, w);
-    return cudaGetLastError();
+    return launch_kernel(kernel, grid, kBlock, smem, st, a, w);
 }
 
 }  // namespace

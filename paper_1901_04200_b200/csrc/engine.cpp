@@ -24,10 +24,12 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <numeric>
 #include <condition_variable>
+#include <functional>
 #include <thread>
 #include <stdexcept>
 #include <string>
@@ -180,12 +182,172 @@ struct Loopback {
     }
 };
 
+namespace ltg {
+thread_local LaunchHook* t_launch_hook = nullptr;
+}
+
+// CUDA-graph replay of a call on a single-GPU context (run_body). A call's
+// device work — the H2D copy of x and the targets, the counter memsets, the
+// pass kernels, the reductions, the timing events and the D2H copies of the
+// report and the rare flag — is captured into a graph the second time a call
+// of the same shape arrives; later calls of that shape replay it with one
+// cudaGraphLaunch. The host code of the call still runs, with the hook
+// installed in Update mode: every enqueue is compared with the captured
+// sequence, kernels whose arguments changed (parameters, seed, ...) get their
+// graph node updated (cudaGraphExecKernelNodeSetParams), and any other
+// difference (a buffer moved, a different plan) drops the graph and runs the
+// call eagerly.
+struct GraphRec : LaunchHook {
+    enum Mode { Capture, Update } mode = Capture;
+    struct Kernel {
+        const void* func;
+        dim3 grid, block;
+        size_t smem;
+        std::vector<size_t> sizes;
+        std::vector<char> args;
+    };
+    struct Op {  // memset / copy / event: kind and operands must repeat exactly
+        int kind;
+        const void* a;
+        const void* b;
+        size_t n;
+    };
+    std::vector<Kernel> kernels;
+    std::vector<Op> ops;
+    std::vector<cudaGraphNode_t> knodes;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::string key;
+    size_t kcur = 0, ocur = 0;
+    bool mismatch = false;
+
+    ~GraphRec() override { reset(); }
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+        kernels.clear();
+        ops.clear();
+        knodes.clear();
+        key.clear();
+    }
+    static bool same(dim3 a, dim3 b) { return a.x == b.x && a.y == b.y && a.z == b.z; }
+    cudaError_t launch(const void* func, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       void** args, const size_t* sizes, int n) override {
+        std::vector<size_t> sz(sizes, sizes + n);
+        std::vector<char> bytes;
+        for (int i = 0; i < n; ++i)
+            bytes.insert(bytes.end(), static_cast<char*>(args[i]), static_cast<char*>(args[i]) + sizes[i]);
+        if (mode == Capture) {
+            kernels.push_back({func, grid, block, smem, sz, bytes});
+            return cudaLaunchKernel(func, grid, block, args, smem, st);
+        }
+        if (kcur >= kernels.size()) {
+            mismatch = true;
+            return cudaSuccess;
+        }
+        Kernel& k = kernels[kcur++];
+        if (k.func != func || !same(k.grid, grid) || !same(k.block, block) || k.smem != smem ||
+            k.sizes != sz) {
+            mismatch = true;
+            return cudaSuccess;
+        }
+        if (k.args != bytes && !mismatch) {
+            cudaKernelNodeParams p{};
+            p.func = const_cast<void*>(func);
+            p.gridDim = grid;
+            p.blockDim = block;
+            p.sharedMemBytes = (unsigned)smem;
+            p.kernelParams = args;
+            if (cudaGraphExecKernelNodeSetParams(exec, knodes[kcur - 1], &p) != cudaSuccess) {
+                mismatch = true;
+                cudaGetLastError();
+                return cudaSuccess;
+            }
+            k.args.swap(bytes);
+        }
+        return cudaSuccess;
+    }
+    // non-kernel enqueue: true = enqueue it (eager / capture), false = the graph has it
+    bool op(int kind, const void* a, const void* b, size_t n) {
+        if (mode == Capture) {
+            ops.push_back({kind, a, b, n});
+            return true;
+        }
+        if (ocur >= ops.size() || ops[ocur].kind != kind || ops[ocur].a != a || ops[ocur].b != b ||
+            ops[ocur].n != n)
+            mismatch = true;
+        ++ocur;
+        return false;
+    }
+};
+thread_local GraphRec* t_rec = nullptr;
+
+// persistent worker threads of a multi-device context (group_run): member i
+// > 0 runs on worker i - 1, member 0 on the calling thread
+struct Pool {
+    std::vector<std::thread> threads;
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    std::function<void(size_t)> job;
+    uint64_t gen = 0;
+    size_t pending = 0;
+    bool stop = false;
+    explicit Pool(size_t workers) {
+        for (size_t i = 0; i < workers; ++i)
+            threads.emplace_back([this, i] {
+                uint64_t seen = 0;
+                for (;;) {
+                    std::function<void(size_t)> fn;
+                    {
+                        std::unique_lock<std::mutex> lock(mu);
+                        cv.wait(lock, [&] { return stop || gen != seen; });
+                        if (stop) return;
+                        seen = gen;
+                        fn = job;
+                    }
+                    fn(i + 1);
+                    std::lock_guard<std::mutex> lock(mu);
+                    if (--pending == 0) done_cv.notify_all();
+                }
+            });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : threads) t.join();
+    }
+    // fn(0) on the caller, fn(1..workers) on the workers; returns when all are done
+    void run(const std::function<void(size_t)>& fn) {
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            job = fn;
+            pending = threads.size();
+            ++gen;
+        }
+        cv.notify_all();
+        fn(0);
+        std::unique_lock<std::mutex> lock(mu);
+        done_cv.wait(lock, [&] { return pending == 0; });
+    }
+};
+
 struct ltg_ctx {
     // single-process multi-GPU context (ltg_create_*_devices): one member
     // context per device, member i = NCCL rank i; the group itself has no
     // device state and runs every call on all members concurrently
     std::vector<std::unique_ptr<ltg_ctx>> members;
+    std::unique_ptr<Pool> pool;      // the members' host threads (members.size() - 1 workers)
     std::shared_ptr<Loopback> loop;  // test-only collective instead of NCCL (see Loopback)
+    // call graphs by call shape (run_body): seen once -> captured on the
+    // next call -> replayed; a few shapes (gradient / means / tangent calls
+    // of a calibration loop) are kept
+    std::map<std::string, std::unique_ptr<GraphRec>> graphs;
+    std::vector<std::string> graph_order;  // insertion order, oldest first
     uint64_t hbm_budget = 0;         // ltg_set_hbm_budget: cap of checkpoints + draws (0: free HBM)
     int kind = 0;  // 0 Heston SLV, 1 basket
     uint64_t path_base = 0;  // global index of path 0 of a call (ltg_chunk_sums; else 0)
@@ -286,18 +448,15 @@ void require(bool ok, const std::string& msg) {
 bool is_group(const ltg_ctx* c) { return c && !c->members.empty(); }
 
 // Run fn(member, index) on every member of a multi-GPU context, one host
-// thread per device (their NCCL collectives meet), and report the first
-// failure. Validation failures happen identically on every member before any
+// thread per device (their NCCL collectives meet; the threads persist with
+// the context), and report the first failure. Validation failures happen identically on every member before any
 // collective, so a bad argument cannot leave some members waiting.
 template <typename Fn>
 int group_run(ltg_ctx* g, Fn&& fn) {
     const size_t n = g->members.size();
     std::vector<int> rc(n, LTG_OK);
-    std::vector<std::thread> threads;
-    for (size_t i = 1; i < n; ++i)
-        threads.emplace_back([&, i] { rc[i] = fn(g->members[i].get(), i); });
-    rc[0] = fn(g->members[0].get(), size_t(0));
-    for (auto& t : threads) t.join();
+    if (!g->pool) g->pool = std::make_unique<Pool>(n - 1);
+    g->pool->run([&](size_t i) { rc[i] = fn(g->members[i].get(), i); });
     for (size_t i = 0; i < n; ++i)
         if (rc[i] != LTG_OK) {
             g->err = g->members[i]->err;
@@ -558,9 +717,25 @@ Work base_work(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan) {
     return w;
 }
 
+// Enqueue helpers of a call's non-kernel device work (see GraphRec).
+void enq_memset(ltg_ctx* c, void* p, size_t n) {
+    if (t_rec && !t_rec->op(0, p, nullptr, n)) return;
+    cuda_check(cudaMemsetAsync(p, 0, n, c->stream), "memset");
+}
+void enq_copy(ltg_ctx* c, void* dst, const void* src, size_t n, cudaMemcpyKind kind) {
+    if (t_rec && !t_rec->op(1 + (int)kind, dst, src, n)) return;
+    cuda_check(cudaMemcpyAsync(dst, src, n, kind, c->stream), "copy");
+}
+void rec_event(ltg_ctx* c, int i) {
+    if (t_rec && !t_rec->op(16, c->ev[i], nullptr, 0)) return;
+    // (inside a capture: an event-record node, so the timing events work on replay)
+    cuda_check(t_rec ? cudaEventRecordWithFlags(c->ev[i], c->stream, cudaEventRecordExternal)
+                     : cudaEventRecord(c->ev[i], c->stream),
+               "event");
+}
+
 void zero_counter(ltg_ctx* c, int slot) {
-    cuda_check(cudaMemsetAsync(c->d_counter.as<uint32_t>() + slot, 0, sizeof(uint32_t), c->stream),
-               "memset");
+    enq_memset(c, c->d_counter.as<uint32_t>() + slot, sizeof(uint32_t));
 }
 
 void validate_cfg(ltg_ctx* c, const ltg_mc_config* cfg, size_t M) {
@@ -619,9 +794,9 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         b.write_sums = 1;
         b.write_store = c->store_ok ? 1 : 0;
         zero_counter(c, 0);
-        cuda_check(cudaEventRecord(c->ev[0], c->stream), "event");
+        rec_event(c, 0);
         if (w.n_chunks) cuda_check(launch_basket_pass1(b, w, 0, c->stream), "basket pass 1");
-        cuda_check(cudaEventRecord(c->ev[1], c->stream), "event");
+        rec_event(c, 1);
         c->timing.launches += w.n_chunks ? 1 : 0;
     }
     // HBM plan for pass 2's inputs: the state every KS steps,
@@ -715,9 +890,9 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         a.z_stride = std::max<uint64_t>(1, c->z_chunks * plan.chunk_paths);
         a.write_z = c->z_chunks > 0 ? 1 : 0;
         zero_counter(c, 0);
-        cuda_check(cudaEventRecord(c->ev[0], c->stream), "event");
+        rec_event(c, 0);
         if (w.n_chunks) cuda_check(launch_heston_pass1(a, w, 0, c->stream), "heston pass 1");
-        cuda_check(cudaEventRecord(c->ev[1], c->stream), "event");
+        rec_event(c, 1);
         c->timing.launches += w.n_chunks ? 1 : 0;
     } else {
         ckpt = c->store_ok;
@@ -733,7 +908,7 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                                     c->d_groups.as<double>(), c->d_tot1.as<double>(), fin,
                                     c->stream),
                "reduce");
-    cuda_check(cudaEventRecord(c->ev[2], c->stream), "event");
+    rec_event(c, 2);
     c->timing.launches += 2;
     c->timing.paths_pass1 = plan.path_end - plan.path_begin;
     if (ckpt && c->kind == 0) {
@@ -766,7 +941,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     a.draws_row0 = p2_row0;
     Work w = base_work(c, cfg, plan);
     const uint32_t nseg = (c->steps + c->seg_steps - 1) / c->seg_steps;
-    cuda_check(cudaEventRecord(c->ev[3], c->stream), "event");
+    rec_event(c, 3);
     if (w.n_chunks && c->kind == 1) {
         BasketArgs b = basket_args(c, c->h_x.data());
         b.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
@@ -860,7 +1035,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
             c->timing.launches += 1;
         }
     }
-    cuda_check(cudaEventRecord(c->ev[4], c->stream), "event");
+    rec_event(c, 4);
     all_gather_rows(c, c->d_part2.as<double>(), per, c->M);
     Finish fin{};
     fin.grad = 1;
@@ -871,7 +1046,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                                     c->d_groups.as<double>(), c->d_tot2.as<double>(), fin,
                                     c->stream),
                "reduce");
-    cuda_check(cudaEventRecord(c->ev[5], c->stream), "event");
+    rec_event(c, 5);
     c->timing.launches += 2;
     c->timing.paths_pass2 = plan.path_end - plan.path_begin;
 }
@@ -896,9 +1071,9 @@ void run_tangent(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bo
     if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
     zero_counter(c, 2);
     w.counter = c->d_counter.as<uint32_t>() + 2;
-    cuda_check(cudaEventRecord(c->ev[sums ? 0 : 3], c->stream), "event");
+    rec_event(c, sums ? 0 : 3);
     if (w.n_chunks) cuda_check(launch_heston_tangent(a, w, 0, c->stream), "heston tangent");
-    cuda_check(cudaEventRecord(c->ev[sums ? 1 : 4], c->stream), "event");
+    rec_event(c, sums ? 1 : 4);
     c->timing.launches += w.n_chunks ? 1 : 0;
     all_gather_rows(c, c->d_part2.as<double>(), per, width);
     // one finishing launch: (means, lambda, G when this launch is pass 1) then
@@ -919,11 +1094,11 @@ void run_tangent(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bo
     c->timing.launches += 2;
     if (sums) {
         c->timing.paths_pass1 = plan.path_end - plan.path_begin;
-        cuda_check(cudaEventRecord(c->ev[2], c->stream), "event");
-        cuda_check(cudaEventRecord(c->ev[3], c->stream), "event");
-        cuda_check(cudaEventRecord(c->ev[4], c->stream), "event");
+        rec_event(c, 2);
+        rec_event(c, 3);
+        rec_event(c, 4);
     }
-    cuda_check(cudaEventRecord(c->ev[5], c->stream), "event");
+    rec_event(c, 5);
     c->timing.paths_pass2 = plan.path_end - plan.path_begin;
 }
 
@@ -946,37 +1121,33 @@ int start_safe(const ltg_ctx* c) {
 }
 
 void clear_rare(ltg_ctx* c) {
-    cuda_check(cudaMemsetAsync(c->d_counter.as<uint32_t>() + kRareSlot, 0, sizeof(uint32_t),
-                               c->stream),
-               "memset");
+    enq_memset(c, c->d_counter.as<uint32_t>() + kRareSlot, sizeof(uint32_t));
 }
 
-bool take_rare(ltg_ctx* c, double* host_slot) {
+// The rare flag after the call's kernels: all-reduced over the ranks (NCCL)
+// and copied to host_slot (enqueue_rare), then read once the stream is done
+// (wait_rare; loopback members exchange it on the host instead).
+void enqueue_rare(ltg_ctx* c, double* host_slot) {
     uint32_t* d = c->d_counter.as<uint32_t>() + kRareSlot;
-    if (c->loop) {
-        Loopback& L = *c->loop;
-        uint32_t v = 0;
-        cuda_check(cudaMemcpyAsync(host_slot, d, sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                                   c->stream),
-                   "D2H");
-        cuda_check(cudaStreamSynchronize(c->stream), "synchronize");
-        std::memcpy(&v, host_slot, sizeof v);
-        L.flags[c->rank] = v;
-        L.barrier();
-        for (uint32_t f : L.flags) v = std::max(v, f);
-        L.barrier();
-        return v != 0;
-    }
-    if (c->comm) {
+    if (c->comm && !c->loop) {
         const ncclResult_t r = nccl().AllReduce(d, d, 1, ncclUint32, ncclMax, c->comm, c->stream);
         if (r != ncclSuccess)
             throw Failure(LTG_ECUDA, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
     }
-    cuda_check(cudaMemcpyAsync(host_slot, d, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream),
-               "D2H");
+    enq_copy(c, host_slot, d, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+}
+
+bool wait_rare(ltg_ctx* c, const double* host_slot) {
     cuda_check(cudaStreamSynchronize(c->stream), "synchronize");
     uint32_t v = 0;
     std::memcpy(&v, host_slot, sizeof v);
+    if (c->loop) {
+        Loopback& L = *c->loop;
+        L.flags[c->rank] = v;
+        L.barrier();
+        for (uint32_t f : L.flags) v = std::max(v, f);
+        L.barrier();
+    }
     return v != 0;
 }
 
@@ -987,13 +1158,112 @@ void upload_x(ltg_ctx* c, const double* x, const double* targets) {
     std::memcpy(st, x, c->M * 8);
     if (targets) std::memcpy(st + c->M, targets, c->m * 8);
     c->d_x.ensure(c->M * 8);
-    cuda_check(cudaMemcpyAsync(c->d_x.p, st, c->M * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    enq_copy(c, c->d_x.p, st, c->M * 8, cudaMemcpyHostToDevice);
     if (targets) {
         c->d_targets.ensure(c->m * 8);
-        cuda_check(cudaMemcpyAsync(c->d_targets.p, st + c->M, c->m * 8, cudaMemcpyHostToDevice,
-                                   c->stream),
-                   "H2D");
+        enq_copy(c, c->d_targets.p, st + c->M, c->m * 8, cudaMemcpyHostToDevice);
     }
+}
+
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("LTG_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// Runs the enqueue sequence `body` of one call: eagerly; or, for a
+// single-GPU context whose call of shape `key` arrives the second time in a
+// row, captured into a graph and launched; or, for later calls of that
+// shape, as an update of the graph followed by one cudaGraphLaunch (GraphRec).
+void run_body(ltg_ctx* c, bool graphable, const std::string& key,
+              const std::function<void()>& body) {
+    if (!graphable || !graphs_enabled()) {
+        body();
+        return;
+    }
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {  // first call of this shape: eager (allocates, plans)
+        constexpr size_t kMaxGraphs = 8;
+        if (c->graph_order.size() == kMaxGraphs) {
+            c->graphs.erase(c->graph_order.front());
+            c->graph_order.erase(c->graph_order.begin());
+        }
+        c->graphs.emplace(key, std::make_unique<GraphRec>());
+        c->graph_order.push_back(key);
+        body();
+        return;
+    }
+    GraphRec& g = *it->second;
+    struct Hook {
+        explicit Hook(GraphRec* r) { t_rec = r; t_launch_hook = r; }
+        ~Hook() { t_rec = nullptr; t_launch_hook = nullptr; }
+    };
+    if (g.exec && g.key == key) {
+        const ltg_timing saved = c->timing;
+        g.mode = GraphRec::Update;
+        g.kcur = g.ocur = 0;
+        g.mismatch = false;
+        {
+            Hook h(&g);
+            body();
+        }
+        if (!g.mismatch && g.kcur == g.kernels.size() && g.ocur == g.ops.size()) {
+            cuda_check(cudaGraphLaunch(g.exec, c->stream), "cudaGraphLaunch");
+            c->timing.graph = 2;
+            return;
+        }
+        g.reset();  // the call's shape changed under the same key: eager, recapture next time
+        c->timing = saved;
+        body();
+        return;
+    }
+    g.reset();
+    g.mode = GraphRec::Capture;
+    cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "capture");
+    try {
+        Hook h(&g);
+        body();
+    } catch (...) {
+        cudaGraph_t dead = nullptr;
+        cudaStreamEndCapture(c->stream, &dead);
+        if (dead) cudaGraphDestroy(dead);
+        cudaGetLastError();
+        g.reset();
+        throw;
+    }
+    cuda_check(cudaStreamEndCapture(c->stream, &g.graph), "end capture");
+    // the capture of one stream is a chain: its kernel nodes in launch order
+    size_t nroot = 0;
+    cuda_check(cudaGraphGetRootNodes(g.graph, nullptr, &nroot), "graph roots");
+    std::vector<cudaGraphNode_t> cur(nroot);
+    cuda_check(cudaGraphGetRootNodes(g.graph, cur.data(), &nroot), "graph roots");
+    while (cur.size() == 1) {
+        cudaGraphNodeType t;
+        cuda_check(cudaGraphNodeGetType(cur[0], &t), "node type");
+        if (t == cudaGraphNodeTypeKernel) g.knodes.push_back(cur[0]);
+        size_t nd = 0;
+        cuda_check(cudaGraphNodeGetDependentNodes(cur[0], nullptr, &nd), "dependents");
+        std::vector<cudaGraphNode_t> next(nd);
+        if (nd) cuda_check(cudaGraphNodeGetDependentNodes(cur[0], next.data(), &nd), "dependents");
+        cur.swap(next);
+    }
+    if (!cur.empty() || g.knodes.size() != g.kernels.size()) {
+        // not the expected chain: run this call from the captured graph
+        // once, keep no graph
+        cudaGraphExec_t once = nullptr;
+        cuda_check(cudaGraphInstantiate(&once, g.graph, 0), "instantiate");
+        cuda_check(cudaGraphLaunch(once, c->stream), "cudaGraphLaunch");
+        cuda_check(cudaStreamSynchronize(c->stream), "synchronize");
+        cudaGraphExecDestroy(once);
+        g.reset();
+        return;
+    }
+    cuda_check(cudaGraphInstantiate(&g.exec, g.graph, 0), "instantiate");
+    g.key = key;
+    cuda_check(cudaGraphLaunch(g.exec, c->stream), "cudaGraphLaunch");
+    c->timing.graph = 1;
 }
 
 }  // namespace
@@ -1355,33 +1625,38 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
                     "fp32 gradient_of_G needs the Feller condition 2*kappa*theta >= xi^2 "
                     "(its accuracy bar is not met at the variance truncation kink); use fp64");
         const uint32_t nm = ctx->m;
-        double* st = nullptr;
+        // one pinned staging area per call: x and the targets in, the report
+        // and the rare flag out (sized up front: a graph captures its address)
+        double* st = ctx->stage(std::max<size_t>(ctx->M + nm, 2 + 3 * nm + ctx->M));
+        const bool graphable = !src && !ctx->comm && !ctx->loop && ctx->world == 1 &&
+                               !cfg->fresh_step2_paths;
+        const std::string key = std::string(tangent ? "tangent" : "grad") + "/" +
+                                std::to_string(cfg->paths) + "/" + std::to_string(cfg->antithetic) +
+                                "/" + std::to_string(cfg->precision);
         // (caller draws run the exact slow paths from the start: DrawScope)
         for (ctx->safe = src ? 1 : start_safe(ctx);; ctx->safe = 1) {
             const uint32_t rerun = ctx->safe && !src && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
             ctx->timing.safe_rerun = rerun;
-            upload_x(ctx, x, targets);
-            clear_rare(ctx);
-            if (tangent) {
-                if (cfg->fresh_step2_paths) {
-                    run_pass1(ctx, *cfg, plan, true, false);
-                    run_tangent(ctx, *cfg, plan, false);
+            run_body(ctx, graphable && !ctx->safe, key, [&] {
+                upload_x(ctx, x, targets);
+                clear_rare(ctx);
+                if (tangent) {
+                    if (cfg->fresh_step2_paths) {
+                        run_pass1(ctx, *cfg, plan, true, false);
+                        run_tangent(ctx, *cfg, plan, false);
+                    } else {
+                        run_tangent(ctx, *cfg, plan, true);
+                    }
                 } else {
-                    run_tangent(ctx, *cfg, plan, true);
+                    const bool ckpt = run_pass1(ctx, *cfg, plan, true, !cfg->fresh_step2_paths);
+                    run_pass2(ctx, *cfg, plan, ckpt);
                 }
-            } else {
-                const bool ckpt = run_pass1(ctx, *cfg, plan, true, !cfg->fresh_step2_paths);
-                run_pass2(ctx, *cfg, plan, ckpt);
-            }
-            st = ctx->stage(2 + 3 * nm + ctx->M);
-            cuda_check(cudaMemcpyAsync(st, ctx->d_res.p, (1 + 3 * nm) * 8,
-                                       cudaMemcpyDeviceToHost, ctx->stream),
-                       "D2H");
-            cuda_check(cudaMemcpyAsync(st + 1 + 3 * nm, ctx->d_grad.p, ctx->M * 8,
-                                       cudaMemcpyDeviceToHost, ctx->stream),
-                       "D2H");
-            if (!take_rare(ctx, st + 1 + 3 * nm + ctx->M) || ctx->safe) break;
+                enq_copy(ctx, st, ctx->d_res.p, (1 + 3 * nm) * 8, cudaMemcpyDeviceToHost);
+                enq_copy(ctx, st + 1 + 3 * nm, ctx->d_grad.p, ctx->M * 8, cudaMemcpyDeviceToHost);
+                enqueue_rare(ctx, st + 1 + 3 * nm + ctx->M);
+            });
+            if (!wait_rare(ctx, st + 1 + 3 * nm + ctx->M) || ctx->safe) break;
         }
         ctx->safe = 0;
         ctx->timing.pass1_ms = elapsed(ctx->ev[0], ctx->ev[1]);
@@ -1437,6 +1712,7 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
         check_params(ctx, x);
         ltg_mc_config cfg{npaths, seed, antithetic, 0, 0, LTG_FP64};
         const ltg_shard plan = make_plan(npaths, 0, 1);
+        ctx->stage(std::max<size_t>(M, 2 * m + M + 1));  // (no reallocation mid-call)
         struct Reset {
             ltg_ctx* c;
             ~Reset() { c->path_base = 0; }
@@ -1461,7 +1737,8 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
             cuda_check(cudaMemcpyAsync(st + 2 * m, ctx->d_tot2.p, M * 8, cudaMemcpyDeviceToHost,
                                        ctx->stream),
                        "D2H");
-            if (!take_rare(ctx, st + 2 * m + M) || ctx->safe) {
+            enqueue_rare(ctx, st + 2 * m + M);
+            if (!wait_rare(ctx, st + 2 * m + M) || ctx->safe) {
                 std::memcpy(sums, st, m * 8);
                 std::memcpy(sumsq, st + m, m * 8);
                 std::memcpy(adjoint, st + 2 * m, M * 8);
@@ -1491,20 +1768,24 @@ int means_impl(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
         const DrawScope draws(ctx, src, *cfg, plan);
         const uint32_t nm = ctx->m;
-        double* st = nullptr;
+        double* st = ctx->stage(std::max<size_t>(ctx->M, 2 + 3 * nm));
+        const bool graphable = !src && !ctx->comm && !ctx->loop && ctx->world == 1;
+        const std::string key = "means/" + std::to_string(cfg->paths) + "/" +
+                                std::to_string(cfg->antithetic) + "/" +
+                                std::to_string(cfg->precision);
         // (caller draws run the exact slow paths from the start: DrawScope)
         for (ctx->safe = src ? 1 : start_safe(ctx);; ctx->safe = 1) {
             const uint32_t rerun = ctx->safe && !src && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
             ctx->timing.safe_rerun = rerun;
-            upload_x(ctx, x, nullptr);
-            clear_rare(ctx);
-            run_pass1(ctx, *cfg, plan, false, false);
-            st = ctx->stage(2 + 3 * nm);
-            cuda_check(cudaMemcpyAsync(st, ctx->d_res.p, (1 + 3 * nm) * 8,
-                                       cudaMemcpyDeviceToHost, ctx->stream),
-                       "D2H");
-            if (!take_rare(ctx, st + 1 + 3 * nm) || ctx->safe) break;
+            run_body(ctx, graphable && !ctx->safe, key, [&] {
+                upload_x(ctx, x, nullptr);
+                clear_rare(ctx);
+                run_pass1(ctx, *cfg, plan, false, false);
+                enq_copy(ctx, st, ctx->d_res.p, (1 + 3 * nm) * 8, cudaMemcpyDeviceToHost);
+                enqueue_rare(ctx, st + 1 + 3 * nm);
+            });
+            if (!wait_rare(ctx, st + 1 + 3 * nm) || ctx->safe) break;
         }
         ctx->safe = 0;
         ctx->timing.pass1_ms = elapsed(ctx->ev[0], ctx->ev[1]);

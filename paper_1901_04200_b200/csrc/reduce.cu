@@ -162,10 +162,11 @@ cudaError_t launch_reduce_chunks(const double* table, uint64_t n_chunks, uint32_
                                  double* group_scratch, double* out, const Finish& fin,
                                  cudaStream_t s) {
     const uint64_t n_groups = (n_chunks + kGroup - 1) / kGroup;
-    reduce_groups_kernel<<<(unsigned)n_groups, kFinishThreads, 0, s>>>(table, n_chunks, width,
-                                                                        group_scratch);
-    reduce_final_kernel<<<1, kFinishThreads, 0, s>>>(group_scratch, n_groups, width, out, fin);
-    return cudaGetLastError();
+    const cudaError_t e = launch_kernel(reduce_groups_kernel, (unsigned)n_groups, kFinishThreads,
+                                        0, s, table, n_chunks, width, group_scratch);
+    if (e != cudaSuccess) return e;
+    return launch_kernel(reduce_final_kernel, 1, kFinishThreads, 0, s, (const double*)group_scratch,
+                         n_groups, width, out, fin);
 }
 
 cudaError_t launch_fill_normals(const RngTables* tables, const RngConsts& rc, uint32_t seed_lo,

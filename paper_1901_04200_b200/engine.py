@@ -252,6 +252,28 @@ class Engine:
             out.std_errors = se.tolist()
         return out
 
+    def prepared_gradient(self, x, targets, cfg: MCConfig):
+        """A bound ltg_gradient_of_G call on fixed host buffers (what a C / C++
+        caller of the ABI holds): returns (call, xbuf, tbuf, out) where call()
+        runs the two-pass gradient on the current contents of the host
+        arrays xbuf / tbuf and leaves G, means, lambda and grad in `out`
+        (bench.py's end-to-end timing: no per-call Python marshalling)."""
+        xb, tb = _arr(x).copy(), _arr(targets).copy()
+        out = {"means": np.empty(self.m), "lambda": np.empty(self.m), "grad": np.empty(self.M)}
+        rep = ReportC(0.0, _p(out["means"]), _p(out["lambda"]), _p(out["grad"]), None, 0, 0, 0)
+        c = _cfg(cfg)
+        fn, h, lib = self.lib.ltg_gradient_of_G, self.h, self
+        args = (h, _p(xb), xb.size, _p(tb), tb.size, C.byref(c), C.byref(rep))
+
+        def call():
+            rc = fn(*args)
+            if rc:
+                lib._raise(rc)
+            return rep.G
+
+        out["report"] = rep
+        return call, xb, tb, out
+
     def estimate_means(self, x, cfg, source=None, paths: Optional[int] = None) -> MeansResult:
         """expectation.hpp:281-286 (Philox draws from cfg.seed); with
         ``source=BufferDrawSource`` and ``paths`` the PathDrawSource overload

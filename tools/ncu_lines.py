@@ -1,6 +1,6 @@
 """Attribute ncu per-SASS stall samples / executed instructions to source lines.
 
-usage: ncu_lines.py <report.ncu-rep> <kernel-regex> <engine .so> [top]
+usage: ncu_lines.py <report.ncu-rep | source-page.csv[.gz]> <kernel-regex> <engine .so> [top]
 Joins `ncu --page source --print-source sass` (per-address samples) with the
 line table of `nvdisasm -g` on the cubin inside the .so (needs -lineinfo)."""
 import collections, csv, glob, io, os, re, subprocess, sys, tempfile
@@ -8,9 +8,13 @@ import collections, csv, glob, io, os, re, subprocess, sys, tempfile
 rep, kern, so = sys.argv[1], sys.argv[2], os.path.abspath(sys.argv[3])
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
-                      f"regex:{kern}", "--print-source", "sass"], capture_output=True,
-                     text=True).stdout.splitlines()
+if rep.endswith(".csv") or rep.endswith(".csv.gz"):  # an exported source page (gpu_profile.sh)
+    import gzip
+    out = (gzip.open(rep, "rt") if rep.endswith(".gz") else open(rep)).read().splitlines()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
+                          f"regex:{kern}", "--print-source", "sass"], capture_output=True,
+                         text=True).stdout.splitlines()
 kname = None
 rows = []
 hdr = None
@@ -18,8 +22,11 @@ for l in out:
     r = next(csv.reader([l]))
     if r and r[0] == "Kernel Name":
         if kname is not None:
-            break  # first kernel only
-        kname = r[1]
+            break  # first matching kernel only
+        if re.search(kern, r[1]):
+            kname = r[1]
+        continue
+    if kname is None:
         continue
     if r and r[0] == "Address":
         hdr = r
@@ -32,10 +39,21 @@ base = rows[0][0]
 
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
-m = re.search(r"heston_(pass\d)_kernel<(double|float), (?:\(int\))?(\d+), (?:\(bool\))?(\d)>",
-              kname)
-want = (f"heston_{m.group(1)}_kernelI{m.group(2)[0]}Li{m.group(3)}ELb{m.group(4)}E" if m
-        else kern)
+# demangled template arguments -> the mangled name's argument list, e.g.
+# heston_pass1_kernel<double, (int)8, (int)3, (bool)0, (bool)0> -> heston_pass1_kernelIdLi8ELi3ELb0ELb0E
+m = re.search(r"(\w+_kernel)<([^>]*)>", kname)
+want = kern
+if m:
+    parts = []
+    for a in m.group(2).split(","):
+        a = a.strip()
+        if a in ("double", "float"):
+            parts.append(a[0])
+        else:
+            mm = re.match(r"\((int|bool)\)(-?\d+)", a)
+            if mm:
+                parts.append(("Li" if mm.group(1) == "int" else "Lb") + mm.group(2) + "E")
+    want = m.group(1) + "I" + "".join(parts) + "E"
 lines = {}
 for cub in glob.glob(os.path.join(tmp, "*.cubin")):
     dis = subprocess.run(["nvdisasm", "-g", cub], capture_output=True, text=True).stdout
