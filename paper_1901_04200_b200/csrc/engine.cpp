@@ -250,6 +250,9 @@ struct GraphRec : LaunchHook {
         Kernel& k = kernels[kcur++];
         if (k.func != func || !same(k.grid, grid) || !same(k.block, block) || k.smem != smem ||
             k.sizes != sz) {
+            if (std::getenv("LTG_GRAPH_DEBUG"))
+                std::fprintf(stderr, "graph: kernel %zu differs (func %d grid %d smem %d)\n",
+                             kcur - 1, k.func != func, !same(k.grid, grid), k.smem != smem);
             mismatch = true;
             return cudaSuccess;
         }
@@ -260,7 +263,11 @@ struct GraphRec : LaunchHook {
             p.blockDim = block;
             p.sharedMemBytes = (unsigned)smem;
             p.kernelParams = args;
-            if (cudaGraphExecKernelNodeSetParams(exec, knodes[kcur - 1], &p) != cudaSuccess) {
+            const cudaError_t e = cudaGraphExecKernelNodeSetParams(exec, knodes[kcur - 1], &p);
+            if (e != cudaSuccess) {
+                if (std::getenv("LTG_GRAPH_DEBUG"))
+                    std::fprintf(stderr, "graph: kernel node %zu update failed: %s\n", kcur - 1,
+                                 cudaGetErrorString(e));
                 mismatch = true;
                 cudaGetLastError();
                 return cudaSuccess;
@@ -276,8 +283,11 @@ struct GraphRec : LaunchHook {
             return true;
         }
         if (ocur >= ops.size() || ops[ocur].kind != kind || ops[ocur].a != a || ops[ocur].b != b ||
-            ops[ocur].n != n)
+            ops[ocur].n != n) {
+            if (std::getenv("LTG_GRAPH_DEBUG"))
+                std::fprintf(stderr, "graph: op %zu (kind %d, %zu bytes) differs\n", ocur, kind, n);
             mismatch = true;
+        }
         ++ocur;
         return false;
     }

@@ -25,7 +25,8 @@ for name, paths in (("cfg1", 1 << 16), ("cfg3", 4099), ("cfg4", 3001)):
     t = configs.load_targets(c) or c.targets
     eng = Engine(c.spec)
     x1 = list(c.x)
-    x2 = [v * 1.01 for v in c.x]
+    # (x2 keeps config 3's unit leverage cell: L = 1.0 selects other kernels)
+    x2 = [v * 1.01 for v in c.x[:5]] + list(c.x[5:]) if name == "cfg3" else [v * 1.01 for v in c.x]
     calls = [(x1, 7, paths), (x1, 7, paths), (x1, 7, paths), (x2, 7, paths), (x2, 8, paths),
              (x1, 9, paths + 128), (x1, 9, paths + 128), (x2, 1, paths + 128), (x1, 7, paths)]
     for i, (x, seed, p) in enumerate(calls):
