@@ -145,9 +145,12 @@ ltg_shard make_plan(uint64_t paths, int rank, int world) {
     return s;
 }
 
-// d_counter slots: 0-2 chunk schedulers of the launches, kRareSlot the
-// fast-arithmetic out-of-range flag
-constexpr int kRareSlot = 8;
+// Per-context call block (d_res): the report a call copies back in one D2H
+// copy, followed by the call's flag words, cleared by one memset:
+//   [G | means m | std_errors m | lambda m | grad M] doubles, then
+//   uint32 flags[16]: flags[0] the fast arithmetic's out-of-range flag,
+//   flags[1 + s] the dynamic chunk scheduler of launch slot s (0-2)
+constexpr int kFlagWords = 16;
 
 uint64_t chunks_per_rank(const ltg_shard& s, int world) {
     return (s.n_chunks + world - 1) / world;
@@ -391,7 +394,7 @@ struct ltg_ctx {
     int safe = 0;             // 1: exact slow paths for every argument (heston_step SAFE)
 
     // per-call buffers
-    DevBuf d_x, d_targets, d_part1, d_part2, d_groups, d_tot1, d_tot2, d_res, d_grad, d_counter,
+    DevBuf d_x, d_part1, d_part2, d_groups, d_tot1, d_tot2, d_res,
         d_ckpt, d_ztab, d_normals;
     uint64_t z_chunks = 0;  // leading local chunks whose draws pass 1 stored
     // caller-supplied draws of the current *_draws call (DrawScope): rows
@@ -412,6 +415,8 @@ struct ltg_ctx {
     // multi-GPU
     int rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    uint32_t fresh_slots = 0;  // scheduler slots zeroed by this call's flag memset, not yet used
+    int timing_pending = 0;    // 1 / 2: `timing`'s device times still to read (settle_timing)
 
     ltg_timing timing{};
 
@@ -436,9 +441,24 @@ struct ltg_ctx {
 
 namespace {
 
+size_t out_doubles(const ltg_ctx* c) { return 1 + 3 * size_t(c->m) + c->M; }
+double* res_ptr(ltg_ctx* c) { return c->d_res.as<double>(); }
+double* grad_ptr(ltg_ctx* c) { return c->d_res.as<double>() + 1 + 3 * size_t(c->m); }
+uint32_t* flags_ptr(ltg_ctx* c) {
+    return reinterpret_cast<uint32_t*>(c->d_res.as<double>() + out_doubles(c));
+}
+uint32_t* rare_ptr(ltg_ctx* c) { return flags_ptr(c); }
+uint32_t* counter_ptr(ltg_ctx* c, int slot) { return flags_ptr(c) + 1 + slot; }
+// the call block, allocated once the model's sizes are known (create)
+void alloc_call_block(ltg_ctx* c) {
+    c->d_res.ensure(out_doubles(c) * 8 + kFlagWords * 4);
+    cuda_check(cudaMemset(c->d_res.p, 0, c->d_res.bytes), "memset");
+}
+
 template <typename Fn>
 int guarded(ltg_ctx* ctx, Fn&& fn) {
     try {
+        if (ctx) ctx->fresh_slots = 0;
         if (ctx && ctx->ready) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         fn();
         return LTG_OK;
@@ -461,6 +481,8 @@ bool is_group(const ltg_ctx* c) { return c && !c->members.empty(); }
 // thread per device (their NCCL collectives meet; the threads persist with
 // the context), and report the first failure. Validation failures happen identically on every member before any
 // collective, so a bad argument cannot leave some members waiting.
+void settle_timing(ltg_ctx* c);
+
 template <typename Fn>
 int group_run(ltg_ctx* g, Fn&& fn) {
     const size_t n = g->members.size();
@@ -472,6 +494,10 @@ int group_run(ltg_ctx* g, Fn&& fn) {
             g->err = g->members[i]->err;
             return rc[i];
         }
+    for (const auto& m : g->members) {
+        cudaSetDevice(m->device);
+        settle_timing(m.get());
+    }
     g->timing = g->members[0]->timing;  // with the slowest member's total
     for (const auto& m : g->members)
         g->timing.total_ms = std::max(g->timing.total_ms, m->timing.total_ms);
@@ -527,7 +553,6 @@ void init_common(ltg_ctx* c, int device) {
     c->d_tab.ensure(sizeof(RngTables));
     cuda_check(cudaMemcpy(c->d_tab.p, &c->h_tab, sizeof(RngTables), cudaMemcpyHostToDevice),
                "rng upload");
-    c->d_counter.ensure(64 * sizeof(uint32_t));
     c->ready = true;
 }
 
@@ -609,7 +634,7 @@ BasketArgs basket_args(ltg_ctx* c, const double* x) {
     a.tables = c->d_tab.as<RngTables>();
     a.rc = c->h_rc;
     a.safe = c->safe;
-    a.rare = c->d_counter.as<uint32_t>() + kRareSlot;
+    a.rare = rare_ptr(c);
     if (c->draws_on) {
         a.draws = c->d_draws.as<double>();
         a.draws_row0 = c->draws_row0A;
@@ -669,7 +694,7 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
     a.unit_lev = (unit_ok && c->nlev == 1 && x[5] == 1.0) ? 1 : 0;
     a.fp32 = c->fp32;
     a.safe = c->safe;
-    a.rare = c->d_counter.as<uint32_t>() + kRareSlot;
+    a.rare = rare_ptr(c);
     a.rare_thr = kRareThr;
     if (c->draws_on) {
         a.draws = c->d_draws.as<double>();
@@ -718,7 +743,7 @@ Work base_work(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan) {
     w.n_chunks = plan.chunk_end - plan.chunk_begin;
     w.ckpt_path0 = plan.path_begin;
     w.ckpt_stride = std::max<uint64_t>(1, plan.path_end - plan.path_begin);
-    w.counter = c->d_counter.as<uint32_t>();
+    w.counter = counter_ptr(c, 0);
     w.seed_lo = (uint32_t)cfg.seed;
     w.seed_hi = (uint32_t)(cfg.seed >> 32);
     // (caller draws: no antithetic pairing, so the kernels' Philox path word
@@ -744,8 +769,14 @@ void rec_event(ltg_ctx* c, int i) {
                "event");
 }
 
+// a scheduler slot before its launch: already zero if the call's flag
+// memset (reset_flags) cleared it and no launch has used it since
 void zero_counter(ltg_ctx* c, int slot) {
-    enq_memset(c, c->d_counter.as<uint32_t>() + slot, sizeof(uint32_t));
+    if (c->fresh_slots & (1u << slot)) {
+        c->fresh_slots &= ~(1u << slot);
+        return;
+    }
+    enq_memset(c, counter_ptr(c, slot), sizeof(uint32_t));
 }
 
 void validate_cfg(ltg_ctx* c, const ltg_mc_config* cfg, size_t M) {
@@ -782,7 +813,6 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     c->d_part1.ensure(table_rows * width * 8);
     c->d_groups.ensure(((plan.n_chunks + kGroup - 1) / kGroup) * std::max(width, c->M) * 8 + 8);
     c->d_tot1.ensure(width * 8);
-    c->d_res.ensure((1 + 3 * c->m) * 8);
 
     Work w = base_work(c, cfg, plan);
     if (c->kind == 1) {
@@ -912,14 +942,14 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     fin.means = 1;
     fin.m = c->m;
     fin.paths = cfg.paths;
-    fin.targets = targets ? c->d_targets.as<double>() : nullptr;
-    fin.res = c->d_res.as<double>();
+    fin.targets = targets ? c->d_x.as<double>() + c->M : nullptr;
+    fin.res = res_ptr(c);
     cuda_check(launch_reduce_chunks(c->d_part1.as<double>(), plan.n_chunks, width,
                                     c->d_groups.as<double>(), c->d_tot1.as<double>(), fin,
                                     c->stream),
                "reduce");
     rec_event(c, 2);
-    c->timing.launches += 2;
+    c->timing.launches += reduce_launch_count(plan.n_chunks);
     c->timing.paths_pass1 = plan.path_end - plan.path_begin;
     if (ckpt && c->kind == 0) {
         c->timing.seg_steps = c->seg_steps;
@@ -936,7 +966,6 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     const uint64_t table_rows = per * c->world;
     c->d_part2.ensure(table_rows * c->M * 8);
     c->d_tot2.ensure(c->M * 8);
-    c->d_grad.ensure(c->M * 8);
     // caller draws: pass 2 reads the rows of its own path set (the fresh
     // step-2 rows follow the pass-1 rows in d_draws)
     const bool fresh_rows = c->draws_on && cfg.fresh_step2_paths;
@@ -946,7 +975,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     const uint64_t p2_row0 = fresh_rows ? c->draws_row0B : c->draws_row0A;
     // (the Heston argument block reads x[0..5]: built for Heston contexts only)
     HestonArgs a = c->kind == 0 ? heston_args(c, c->h_x.data()) : HestonArgs{};
-    a.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
+    a.lambda = res_ptr(c) + 1 + 2 * c->m;
     a.draws = p2_draws;
     a.draws_row0 = p2_row0;
     Work w = base_work(c, cfg, plan);
@@ -954,7 +983,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     rec_event(c, 3);
     if (w.n_chunks && c->kind == 1) {
         BasketArgs b = basket_args(c, c->h_x.data());
-        b.lambda = c->d_res.as<double>() + 1 + 2 * c->m;
+        b.lambda = res_ptr(c) + 1 + 2 * c->m;
         b.draws = p2_draws;
         b.draws_row0 = p2_row0;
         b.partials = c->d_part2.as<double>() + plan.chunk_begin * c->M;
@@ -963,7 +992,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         b.store_stride = w.ckpt_stride;
         if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
         zero_counter(c, 2);
-        w.counter = c->d_counter.as<uint32_t>() + 2;
+        w.counter = counter_ptr(c, 2);
         cuda_check(launch_basket_pass2(b, w, 0, c->stream), "basket pass 2");
         c->timing.launches += 1;
     } else if (w.n_chunks) {
@@ -1001,14 +1030,14 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                 r.check_all = (sf || cfg.fresh_step2_paths) ? 1 : 0;
                 if (cfg.fresh_step2_paths) r.rare_thr = fresh_check_thr();
                 zero_counter(c, 1);
-                ww.counter = c->d_counter.as<uint32_t>() + 1;
+                ww.counter = counter_ptr(c, 1);
                 cuda_check(launch_heston_pass1(r, ww, 0, c->stream), "heston replay");
                 HestonArgs b = a;
                 b.ckpt = c->d_ckpt.p;
                 b.smat = c->d_ckpt.as<char>() + smat_off;
                 b.partials = c->d_part2.as<double>() + ww.chunk_begin * c->M;
                 zero_counter(c, 2);
-                ww.counter = c->d_counter.as<uint32_t>() + 2;
+                ww.counter = counter_ptr(c, 2);
                 cuda_check(launch_heston_pass2(b, ww, 0, c->stream), "heston pass 2");
                 c->timing.launches += 2;
             }
@@ -1027,7 +1056,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                     r.rare_thr = fresh_check_thr();
                     zero_counter(c, 1);
                     Work ww = w;
-                    ww.counter = c->d_counter.as<uint32_t>() + 1;
+                    ww.counter = counter_ptr(c, 1);
                     cuda_check(launch_heston_pass1(r, ww, 0, c->stream), "heston range check");
                     c->timing.launches += 1;
                 }
@@ -1040,7 +1069,7 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
             a.use_z = (c->z_chunks > 0 && !cfg.fresh_step2_paths) ? 1 : 0;
             a.partials = c->d_part2.as<double>() + plan.chunk_begin * c->M;
             zero_counter(c, 2);
-            w.counter = c->d_counter.as<uint32_t>() + 2;
+            w.counter = counter_ptr(c, 2);
             cuda_check(launch_heston_pass2(a, w, 0, c->stream), "heston pass 2");
             c->timing.launches += 1;
         }
@@ -1051,13 +1080,13 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     fin.grad = 1;
     fin.M = (uint32_t)c->M;
     fin.paths = cfg.paths;
-    fin.grad_out = c->d_grad.as<double>();
+    fin.grad_out = grad_ptr(c);
     cuda_check(launch_reduce_chunks(c->d_part2.as<double>(), plan.n_chunks, c->M,
                                     c->d_groups.as<double>(), c->d_tot2.as<double>(), fin,
                                     c->stream),
                "reduce");
     rec_event(c, 5);
-    c->timing.launches += 2;
+    c->timing.launches += reduce_launch_count(plan.n_chunks);
     c->timing.paths_pass2 = plan.path_end - plan.path_begin;
 }
 
@@ -1072,15 +1101,13 @@ void run_tangent(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bo
     c->d_part2.ensure(table_rows * width * 8);
     c->d_groups.ensure(((plan.n_chunks + kGroup - 1) / kGroup) * width * 8 + 8);
     c->d_tot2.ensure(width * 8);
-    c->d_res.ensure((1 + 3 * c->m) * 8);
-    c->d_grad.ensure(c->M * 8);
     HestonArgs a = heston_args(c, c->h_x.data());
     a.partials = c->d_part2.as<double>() + plan.chunk_begin * width;
     a.write_sums = sums ? 1 : 0;
     Work w = base_work(c, cfg, plan);
     if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
     zero_counter(c, 2);
-    w.counter = c->d_counter.as<uint32_t>() + 2;
+    w.counter = counter_ptr(c, 2);
     rec_event(c, sums ? 0 : 3);
     if (w.n_chunks) cuda_check(launch_heston_tangent(a, w, 0, c->stream), "heston tangent");
     rec_event(c, sums ? 1 : 4);
@@ -1094,14 +1121,14 @@ void run_tangent(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bo
     fin.m = c->m;
     fin.M = (uint32_t)c->M;
     fin.paths = cfg.paths;
-    fin.targets = c->d_targets.as<double>();
-    fin.res = c->d_res.as<double>();
-    fin.grad_out = c->d_grad.as<double>();
+    fin.targets = c->d_x.as<double>() + c->M;
+    fin.res = res_ptr(c);
+    fin.grad_out = grad_ptr(c);
     cuda_check(launch_reduce_chunks(c->d_part2.as<double>(), plan.n_chunks, width,
                                     c->d_groups.as<double>(), c->d_tot2.as<double>(), fin,
                                     c->stream),
                "reduce");
-    c->timing.launches += 2;
+    c->timing.launches += reduce_launch_count(plan.n_chunks);
     if (sums) {
         c->timing.paths_pass1 = plan.path_end - plan.path_begin;
         rec_event(c, 2);
@@ -1118,6 +1145,23 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
+// The device times of the last call, read from its events when asked for
+// (ltg_last_timing) rather than inside the call: seven event queries cost
+// more than the whole host side of a replayed small call.
+void settle_timing(ltg_ctx* c) {
+    if (c->timing_pending == 1) {  // gradient_of_G: pass 1, pass 2, both reductions
+        c->timing.pass1_ms = elapsed(c->ev[0], c->ev[1]);
+        c->timing.pass2_ms = elapsed(c->ev[3], c->ev[4]);
+        c->timing.reduce_ms = elapsed(c->ev[1], c->ev[2]) + elapsed(c->ev[4], c->ev[5]);
+        c->timing.total_ms = elapsed(c->ev[0], c->ev[5]);
+    } else if (c->timing_pending == 2) {  // estimate_means: pass 1 and its reduction
+        c->timing.pass1_ms = elapsed(c->ev[0], c->ev[1]);
+        c->timing.reduce_ms = elapsed(c->ev[1], c->ev[2]);
+        c->timing.total_ms = elapsed(c->ev[0], c->ev[2]);
+    }
+    c->timing_pending = 0;
+}
+
 // The fast arithmetic's out-of-range flag (heston.cu heston_step): cleared
 // before a call, OR-ed across ranks, copied back with the results. A set flag
 // makes the caller redo the call in safe mode.
@@ -1130,21 +1174,33 @@ int start_safe(const ltg_ctx* c) {
     return (e && e[0] == '1') || !c->h_rc.exact_exp ? 1 : 0;
 }
 
-void clear_rare(ltg_ctx* c) {
-    enq_memset(c, c->d_counter.as<uint32_t>() + kRareSlot, sizeof(uint32_t));
+// One memset at the start of a call: the rare flag and every scheduler slot.
+void reset_flags(ltg_ctx* c) {
+    enq_memset(c, flags_ptr(c), kFlagWords * 4);
+    c->fresh_slots = 0x7;
 }
 
-// The rare flag after the call's kernels: all-reduced over the ranks (NCCL)
-// and copied to host_slot (enqueue_rare), then read once the stream is done
-// (wait_rare; loopback members exchange it on the host instead).
-void enqueue_rare(ltg_ctx* c, double* host_slot) {
-    uint32_t* d = c->d_counter.as<uint32_t>() + kRareSlot;
+// The rare flag after the call's kernels: all-reduced over the ranks (NCCL);
+// it reaches the host with the report (copy_out), or alone (copy_rare), and
+// is read once the stream is done (wait_rare; loopback members exchange it
+// on the host instead).
+void reduce_rare(ltg_ctx* c) {
+    uint32_t* d = rare_ptr(c);
     if (c->comm && !c->loop) {
         const ncclResult_t r = nccl().AllReduce(d, d, 1, ncclUint32, ncclMax, c->comm, c->stream);
         if (r != ncclSuccess)
             throw Failure(LTG_ECUDA, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
     }
-    enq_copy(c, host_slot, d, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+}
+// the report [G, means, se, lambda, grad] and the rare flag in one copy; the
+// flag lands at host + out_doubles(c)
+void copy_out(ltg_ctx* c, double* host) {
+    reduce_rare(c);
+    enq_copy(c, host, res_ptr(c), out_doubles(c) * 8 + 4, cudaMemcpyDeviceToHost);
+}
+void copy_rare(ltg_ctx* c, double* host_slot) {
+    reduce_rare(c);
+    enq_copy(c, host_slot, rare_ptr(c), 4, cudaMemcpyDeviceToHost);
 }
 
 bool wait_rare(ltg_ctx* c, const double* host_slot) {
@@ -1167,12 +1223,8 @@ void upload_x(ltg_ctx* c, const double* x, const double* targets) {
     double* st = c->stage(n);
     std::memcpy(st, x, c->M * 8);
     if (targets) std::memcpy(st + c->M, targets, c->m * 8);
-    c->d_x.ensure(c->M * 8);
-    enq_copy(c, c->d_x.p, st, c->M * 8, cudaMemcpyHostToDevice);
-    if (targets) {
-        c->d_targets.ensure(c->m * 8);
-        enq_copy(c, c->d_targets.p, st + c->M, c->m * 8, cudaMemcpyHostToDevice);
-    }
+    c->d_x.ensure((c->M + c->m) * 8);  // [x | targets]: one copy
+    enq_copy(c, c->d_x.p, st, n * 8, cudaMemcpyHostToDevice);
 }
 
 bool graphs_enabled() {
@@ -1415,6 +1467,7 @@ int ltg_create_heston(const ltg_heston_model* mdl, int device, ltg_ctx** out) {
         upload(c->d_kind, std::vector<int32_t>(m.inst_kind, m.inst_kind + m.n_instruments));
         build_events(c.get(), std::vector<uint32_t>(m.inst_maturity_step,
                                                      m.inst_maturity_step + m.n_instruments));
+        alloc_call_block(c.get());
         cuda_check(cudaDeviceSynchronize(), "init");
     });
     if (rc != LTG_OK) {
@@ -1474,6 +1527,7 @@ int ltg_create_basket(const ltg_basket_model* mdl, int device, ltg_ctx** out) {
         upload(c->d_asset, std::vector<uint32_t>(m.inst_asset, m.inst_asset + m.n_instruments));
         build_events(c.get(), std::vector<uint32_t>(m.inst_maturity_step,
                                                      m.inst_maturity_step + m.n_instruments));
+        alloc_call_block(c.get());
         cuda_check(cudaDeviceSynchronize(), "init");
     });
     if (rc != LTG_OK) {
@@ -1637,7 +1691,7 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
         const uint32_t nm = ctx->m;
         // one pinned staging area per call: x and the targets in, the report
         // and the rare flag out (sized up front: a graph captures its address)
-        double* st = ctx->stage(std::max<size_t>(ctx->M + nm, 2 + 3 * nm + ctx->M));
+        double* st = ctx->stage(std::max<size_t>(ctx->M + nm, out_doubles(ctx) + 1));
         const bool graphable = !src && !ctx->comm && !ctx->loop && ctx->world == 1 &&
                                !cfg->fresh_step2_paths;
         const std::string key = std::string(tangent ? "tangent" : "grad") + "/" +
@@ -1647,10 +1701,11 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
         for (ctx->safe = src ? 1 : start_safe(ctx);; ctx->safe = 1) {
             const uint32_t rerun = ctx->safe && !src && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
+            ctx->timing_pending = 0;
             ctx->timing.safe_rerun = rerun;
             run_body(ctx, graphable && !ctx->safe, key, [&] {
                 upload_x(ctx, x, targets);
-                clear_rare(ctx);
+                reset_flags(ctx);
                 if (tangent) {
                     if (cfg->fresh_step2_paths) {
                         run_pass1(ctx, *cfg, plan, true, false);
@@ -1662,17 +1717,12 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
                     const bool ckpt = run_pass1(ctx, *cfg, plan, true, !cfg->fresh_step2_paths);
                     run_pass2(ctx, *cfg, plan, ckpt);
                 }
-                enq_copy(ctx, st, ctx->d_res.p, (1 + 3 * nm) * 8, cudaMemcpyDeviceToHost);
-                enq_copy(ctx, st + 1 + 3 * nm, ctx->d_grad.p, ctx->M * 8, cudaMemcpyDeviceToHost);
-                enqueue_rare(ctx, st + 1 + 3 * nm + ctx->M);
+                copy_out(ctx, st);
             });
-            if (!wait_rare(ctx, st + 1 + 3 * nm + ctx->M) || ctx->safe) break;
+            if (!wait_rare(ctx, st + out_doubles(ctx)) || ctx->safe) break;
         }
         ctx->safe = 0;
-        ctx->timing.pass1_ms = elapsed(ctx->ev[0], ctx->ev[1]);
-        ctx->timing.pass2_ms = elapsed(ctx->ev[3], ctx->ev[4]);
-        ctx->timing.reduce_ms = elapsed(ctx->ev[1], ctx->ev[2]) + elapsed(ctx->ev[4], ctx->ev[5]);
-        ctx->timing.total_ms = elapsed(ctx->ev[0], ctx->ev[5]);
+        ctx->timing_pending = 1;  // event times read on demand (settle_timing)
         report->G = st[0];
         std::memcpy(report->means, st + 1, nm * 8);
         if (report->std_errors) std::memcpy(report->std_errors, st + 1 + nm, nm * 8);
@@ -1722,7 +1772,7 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
         check_params(ctx, x);
         ltg_mc_config cfg{npaths, seed, antithetic, 0, 0, LTG_FP64};
         const ltg_shard plan = make_plan(npaths, 0, 1);
-        ctx->stage(std::max<size_t>(M, 2 * m + M + 1));  // (no reallocation mid-call)
+        ctx->stage(std::max<size_t>(M + m, 2 * m + M + 1));  // (no reallocation mid-call)
         struct Reset {
             ltg_ctx* c;
             ~Reset() { c->path_base = 0; }
@@ -1730,10 +1780,11 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
         for (ctx->safe = start_safe(ctx);; ctx->safe = 1) {
             const uint32_t rerun = ctx->safe && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
+            ctx->timing_pending = 0;
             ctx->timing.safe_rerun = rerun;
             ctx->path_base = path0;
             upload_x(ctx, x, nullptr);
-            clear_rare(ctx);
+            reset_flags(ctx);
             const bool ckpt = run_pass1(ctx, cfg, plan, false, true);
             // pass 2 seeded with the caller's lambda instead of pass 1's
             cuda_check(cudaMemcpyAsync(ctx->d_res.as<double>() + 1 + 2 * ctx->m, lambda, m * 8,
@@ -1747,7 +1798,7 @@ int ltg_chunk_sums(ltg_ctx* ctx, const double* x, size_t M, const double* lambda
             cuda_check(cudaMemcpyAsync(st + 2 * m, ctx->d_tot2.p, M * 8, cudaMemcpyDeviceToHost,
                                        ctx->stream),
                        "D2H");
-            enqueue_rare(ctx, st + 2 * m + M);
+            copy_rare(ctx, st + 2 * m + M);
             if (!wait_rare(ctx, st + 2 * m + M) || ctx->safe) {
                 std::memcpy(sums, st, m * 8);
                 std::memcpy(sumsq, st + m, m * 8);
@@ -1778,7 +1829,7 @@ int means_impl(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
         const DrawScope draws(ctx, src, *cfg, plan);
         const uint32_t nm = ctx->m;
-        double* st = ctx->stage(std::max<size_t>(ctx->M, 2 + 3 * nm));
+        double* st = ctx->stage(std::max<size_t>(ctx->M, out_doubles(ctx) + 1));
         const bool graphable = !src && !ctx->comm && !ctx->loop && ctx->world == 1;
         const std::string key = "means/" + std::to_string(cfg->paths) + "/" +
                                 std::to_string(cfg->antithetic) + "/" +
@@ -1787,20 +1838,18 @@ int means_impl(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg
         for (ctx->safe = src ? 1 : start_safe(ctx);; ctx->safe = 1) {
             const uint32_t rerun = ctx->safe && !src && !start_safe(ctx) ? 1u : 0u;
             ctx->timing = ltg_timing{};
+            ctx->timing_pending = 0;
             ctx->timing.safe_rerun = rerun;
             run_body(ctx, graphable && !ctx->safe, key, [&] {
                 upload_x(ctx, x, nullptr);
-                clear_rare(ctx);
+                reset_flags(ctx);
                 run_pass1(ctx, *cfg, plan, false, false);
-                enq_copy(ctx, st, ctx->d_res.p, (1 + 3 * nm) * 8, cudaMemcpyDeviceToHost);
-                enqueue_rare(ctx, st + 1 + 3 * nm);
+                copy_out(ctx, st);
             });
-            if (!wait_rare(ctx, st + 1 + 3 * nm) || ctx->safe) break;
+            if (!wait_rare(ctx, st + out_doubles(ctx)) || ctx->safe) break;
         }
         ctx->safe = 0;
-        ctx->timing.pass1_ms = elapsed(ctx->ev[0], ctx->ev[1]);
-        ctx->timing.reduce_ms = elapsed(ctx->ev[1], ctx->ev[2]);
-        ctx->timing.total_ms = elapsed(ctx->ev[0], ctx->ev[2]);
+        ctx->timing_pending = 2;
         std::memcpy(means, st + 1, nm * 8);
         if (std_errors) std::memcpy(std_errors, st + 1 + nm, nm * 8);
     });
@@ -1972,6 +2021,10 @@ int ltg_set_hbm_budget(ltg_ctx* ctx, uint64_t bytes) {
 
 int ltg_last_timing(const ltg_ctx* ctx, ltg_timing* out) {
     if (!ctx || !out) return LTG_EINVAL;
+    if (ctx->ready && ctx->timing_pending) {
+        cudaSetDevice(ctx->device);
+        settle_timing(const_cast<ltg_ctx*>(ctx));
+    }
     *out = ctx->timing;
     return LTG_OK;
 }

@@ -78,10 +78,7 @@ __device__ void finalize_mean(const double* totals, uint32_t m, uint64_t paths,
 //   grad_tangent: grad[d] = (sum_i lambda_i * J[i][d]) / P, i ascending,
 //          J = totals + 2m, lambda from res (written by `means` above when
 //          both are set).
-__global__ void __launch_bounds__(kFinishThreads) reduce_final_kernel(
-    const double* __restrict__ groups, uint64_t n_groups, uint32_t width, double* out, Finish f) {
-    __shared__ double tile[kTileRows][kTileCols];
-    ordered_column_sums(groups, 0, n_groups, width, out, tile);
+__device__ void finish_call(const double* out, const Finish& f) {
     if (!(f.means || f.grad || f.grad_tangent)) return;
     __syncthreads();  // out visible to the block
     if (f.means) {
@@ -112,6 +109,14 @@ __global__ void __launch_bounds__(kFinishThreads) reduce_final_kernel(
         }
     }
 }
+
+__global__ void __launch_bounds__(kFinishThreads) reduce_final_kernel(
+    const double* __restrict__ groups, uint64_t n_groups, uint32_t width, double* out, Finish f) {
+    __shared__ double tile[kTileRows][kTileCols];
+    ordered_column_sums(groups, 0, n_groups, width, out, tile);
+    finish_call(out, f);
+}
+
 
 // PhiloxNormalSource::fill for a path range through the production
 // generator (gen_segment), one path per thread.
