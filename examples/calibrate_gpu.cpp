@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <span>
 
 #include "lanetape/lanetape.hpp"
 #include "lanetape_b200.hpp"
@@ -40,7 +41,12 @@ int main(int argc, char** argv) {
         const std::vector<double> targets = engine.estimate_means(truth, cfg).means;
 
         const auto g = gpu::make_objective<lt::GradientReport>(engine, targets, cfg);
-        lt::Objective objective{g.value_and_grad, g.value};
+        // count the evaluations the calibrator makes (one gradient_of_G per
+        // iteration, one estimate_means per Armijo trial, calibrate.hpp:149-217)
+        std::size_t n_grad = 0, n_value = 0;
+        lt::Objective objective{
+            [&](std::span<const double> x) { ++n_grad; return g.value_and_grad(x); },
+            [&](std::span<const double> x) { ++n_value; return g.value(x); }};
 
         lt::Bounds bounds{truth, truth};  // frozen at the truth except kappa, theta
         bounds.lo[0] = 1e-3;
@@ -57,17 +63,22 @@ int main(int argc, char** argv) {
         for (std::size_t j = 0; j < truth.size(); ++j)
             opt.scales[j] = std::max(std::abs(truth[j]), 1e-2);
 
+        const auto t1 = std::chrono::steady_clock::now();
         const lt::CalibrationResult res = lt::gradient_descent(objective, x0, bounds, opt);
-        const double sec =
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        const auto t2 = std::chrono::steady_clock::now();
+        const double sec = std::chrono::duration<double>(t2 - t0).count();
+        const double cal = std::chrono::duration<double>(t2 - t1).count();
         const double G0 = res.trajectory.points.front().G;
         std::printf(
             "{\"converged\": %s, \"stop_reason\": \"%s\", \"iters\": %zu, \"G0\": %.17g, "
             "\"G\": %.17g, \"kappa\": %.17g, \"theta\": %.17g, \"kappa_err\": %.3e, "
-            "\"theta_err\": %.3e, \"paths\": %zu, \"seconds\": %.3f}\n",
+            "\"theta_err\": %.3e, \"paths\": %zu, \"seconds\": %.3f, "
+            "\"calibration_seconds\": %.4f, \"gradient_calls\": %zu, \"value_calls\": %zu, "
+            "\"ms_per_evaluation\": %.4f}\n",
             res.converged ? "true" : "false", res.stop_reason.c_str(), res.iters, G0, res.G,
             res.params[0], res.params[1], std::fabs(res.params[0] - truth[0]) / truth[0],
-            std::fabs(res.params[1] - truth[1]) / truth[1], cfg.paths, sec);
+            std::fabs(res.params[1] - truth[1]) / truth[1], cfg.paths, sec, cal, n_grad, n_value,
+            1e3 * cal / double(std::max<std::size_t>(1, n_grad + n_value)));
         return 0;
     } catch (const gpu::EvalError& e) {
         std::fprintf(stderr, "numerical error: %s\n", e.what());

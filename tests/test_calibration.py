@@ -21,3 +21,6 @@ def test_reference_calibrator_recovers_truth_on_gpu(golden_dir):
     assert r["converged"], r
     assert r["G"] <= 1e-10 * r["G0"]
     assert r["kappa_err"] <= 1e-2 and r["theta_err"] <= 1e-2, r
+    # the calibrator's evaluations and their wall time are reported
+    assert r["gradient_calls"] >= r["iters"] and r["value_calls"] >= 0
+    assert 0 < r["ms_per_evaluation"] and r["calibration_seconds"] <= r["seconds"]
