@@ -249,11 +249,6 @@ void fill_as241(RngConsts& K) {
     K.lit_qmax = 0.425;
     K.lit_central = 0.180625;
     K.lit_tail1 = 1.6;
-    for (int s = 0; s < 3; ++s)
-        for (int k = 0; k < 8; ++k) {
-            K.fnum[s][k] = (float)num[s][k];
-            K.fden[s][k] = (float)den[s][k];
-        }
 }
 
 }  // namespace ltg
