@@ -8,7 +8,8 @@ kept them in the HBM draw store and pass 2 reads them); a call's pass-2
 figure is the two weighted by the fraction of its paths whose draws were
 stored (bench.py reads that from ltg_timing.z_bytes).
 Source: profiles/r2_census.txt (cfg3 at 2^20, cfg1 at 2^16, cfg2 and cfg4 at
-2^18 paths; the r2 kernels: S-free pass 2, V-only checkpoints).
+2^18 paths; the r2 kernels: S-free pass 2, V-only checkpoints, the fp32
+mode's single-precision inverse normal).
 
 ALGORITHMIC — EXECUTED minus the kernels' only redundant floating-point work:
 gen_segment evaluates AS241's central branch for every slot of a batch,
@@ -26,8 +27,9 @@ from typing import Dict, Optional, Tuple
 # AS241 central branch per slot (rng.cuh gen_segment phase B): r = c - q*q
 # (2), two degree-7 Horner chains with separate multiply and add (28), q*num
 # (1), the correctly rounded division (8 DFMA/DMUL around MUFU.RCP64H) = 39.
-# fp32 mode: FFMA for r, 14 FFMA, FMUL q*num, FMUL by the MUFU reciprocal = 17.
-CENTRAL_OPS = {"fp64": 39.0, "fp32": 17.0}
+# fp32 mode (the fitted 3/3 rational, f32_normal.h): FFMA for r, 3 + 3 FFMA,
+# FMUL q*num, FMUL by the MUFU reciprocal = 9.
+CENTRAL_OPS = {"fp64": 39.0, "fp32": 9.0}
 TAIL_FRACTION = 0.15  # P(|p - 0.5| > 0.425), p uniform
 
 # name -> (steps, draws per path)
@@ -37,11 +39,11 @@ SHAPE = {"cfg1_gbm": (16, 32), "cfg2_localvol": (64, 128), "cfg3_heston": (756, 
 # (config, precision) -> {kernel: executed instructions per path}
 EXECUTED: Dict[Tuple[str, str], Dict[str, float]] = {
     ("cfg3_heston", "fp64"): {"pass1": 102722.9, "pass2_regen": 106047.7, "pass2_store": 30466.4},
-    ("cfg3_heston", "fp32"): {"pass1": 39733.9, "pass2_regen": 53372.4, "pass2_store": 23586.5},
+    ("cfg3_heston", "fp32"): {"pass1": 28961.1, "pass2_regen": 42713.0, "pass2_store": 23586.5},
     ("cfg1_gbm", "fp64"): {"pass1": 2310.0, "pass2_regen": 2406.8, "pass2_store": 814.1},
-    ("cfg1_gbm", "fp32"): {"pass1": 902.3, "pass2_regen": 1227.4, "pass2_store": 597.1},
+    ("cfg1_gbm", "fp32"): {"pass1": 674.3, "pass2_regen": 1001.9, "pass2_store": 597.1},
     ("cfg2_localvol", "fp64"): {"pass1": 9345.7, "pass2_regen": 11267.9, "pass2_store": 5036.9},
-    ("cfg2_localvol", "fp32"): {"pass1": 3625.4, "pass2_regen": 5438.4, "pass2_store": 2917.1},
+    ("cfg2_localvol", "fp32"): {"pass1": 2713.4, "pass2_regen": 4536.1, "pass2_store": 2917.1},
     # the basket's pass 2 is a store-mode epilogue (no draws, no replay)
     ("cfg4_basket16", "fp64"): {"pass1": 65763.8, "pass2_regen": 455.1, "pass2_store": 455.1},
 }
@@ -50,8 +52,8 @@ EXECUTED: Dict[Tuple[str, str], Dict[str, float]] = {
 DRAM: Dict[Tuple[str, str], Dict[str, float]] = {
     ("cfg3_heston", "fp64"): {"pass1": 753.2, "pass1_store": 12848.5, "pass2_regen": 807.9,
                               "pass2_store": 12908.6},
-    ("cfg3_heston", "fp32"): {"pass1": 351.1, "pass1_store": 6401.7, "pass2_regen": 405.4,
-                              "pass2_store": 6453.1},
+    ("cfg3_heston", "fp32"): {"pass1": 352.0, "pass1_store": 6402.0, "pass2_regen": 406.0,
+                              "pass2_store": 6452.0},
 }
 
 # central-batch widths and normal batches of the kernels (heston.cu: kPass1PB,
