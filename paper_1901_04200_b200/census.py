@@ -39,11 +39,11 @@ SHAPE = {"cfg1_gbm": (16, 32), "cfg2_localvol": (64, 128), "cfg3_heston": (756, 
 # (config, precision) -> {kernel: executed instructions per path}
 EXECUTED: Dict[Tuple[str, str], Dict[str, float]] = {
     ("cfg3_heston", "fp64"): {"pass1": 102722.9, "pass2_regen": 106047.7, "pass2_store": 30466.4},
-    ("cfg3_heston", "fp32"): {"pass1": 28961.1, "pass2_regen": 42713.0, "pass2_store": 23586.5},
+    ("cfg3_heston", "fp32"): {"pass1": 29017.8, "pass2_regen": 42713.0, "pass2_store": 23586.5},
     ("cfg1_gbm", "fp64"): {"pass1": 2310.0, "pass2_regen": 2406.8, "pass2_store": 814.1},
-    ("cfg1_gbm", "fp32"): {"pass1": 674.3, "pass2_regen": 1001.9, "pass2_store": 597.1},
+    ("cfg1_gbm", "fp32"): {"pass1": 675.5, "pass2_regen": 1001.9, "pass2_store": 597.1},
     ("cfg2_localvol", "fp64"): {"pass1": 9345.7, "pass2_regen": 11267.9, "pass2_store": 5036.9},
-    ("cfg2_localvol", "fp32"): {"pass1": 2713.4, "pass2_regen": 4536.1, "pass2_store": 2917.1},
+    ("cfg2_localvol", "fp32"): {"pass1": 2718.2, "pass2_regen": 4536.1, "pass2_store": 2917.1},
     # the basket's pass 2 is a store-mode epilogue (no draws, no replay)
     ("cfg4_basket16", "fp64"): {"pass1": 65763.8, "pass2_regen": 455.1, "pass2_store": 455.1},
 }
