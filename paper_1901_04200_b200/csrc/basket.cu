@@ -31,6 +31,9 @@ namespace {
 
 constexpr int NA = kMaxAssets;
 constexpr int BGS = 16;  // Philox pairs per normal batch (two steps of 16 assets)
+#ifndef LTG_BASKET_FUSED
+#define LTG_BASKET_FUSED LTG_F64_FUSED  // gen_segment's phases A and B fused (rng.cuh)
+#endif
 #ifndef LTG_BPB
 #define LTG_BPB 8  // central slots evaluated together (measured on config 4)
 #endif
@@ -152,8 +155,9 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
         if (DRAWS)  // caller draws: slots [k0*n, k0*n + 2*npairs) of the path's row
             copy_draws<double>(drow, valid, 2 * pair0, 2 * npairs, a.steps * n, zb);
         else
-            gen_segment<BGS, LTG_BPB>(base, neg, pair0, npairs, w.seed_lo, w.seed_hi, zb, wl,
-                                      *s.tab, a.rc);
+            gen_segment<BGS, LTG_BPB, (LTG_BASKET_FUSED != 0)>(base, neg, pair0, npairs,
+                                                               w.seed_lo, w.seed_hi, zb, wl,
+                                                               *s.tab, a.rc);
         for (uint32_t j = 0; j < nb; ++j) {
             const uint32_t k = k0 + j;
             double z[NA];
