@@ -282,6 +282,14 @@ int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int
 
 int ltg_last_timing(const ltg_ctx* ctx, ltg_timing* out);
 
+/* Device timing of calls (ltg_last_timing's pass1_ms / pass2_ms / reduce_ms /
+ * total_ms): on (1, the default) records CUDA events around the passes; off
+ * (0) records none, and those fields read 0. Events cost a small call (or a
+ * replayed graph, whose event-record nodes they become) ~10 us of its ~70,
+ * so latency-bound callers (a calibration loop) switch them off. Results do
+ * not depend on it. */
+int ltg_set_timing(ltg_ctx* ctx, int on);
+
 /* Cap (bytes, per GPU) of the HBM the context may hold for its checkpoint
  * table and draw store; 0 (the default) uses the free device memory minus a
  * 2 GiB reserve. Results do not depend on it, only the speed of pass 2. */

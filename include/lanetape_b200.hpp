@@ -285,6 +285,9 @@ public:
     // HBM cap for the checkpoint table + draw store (0: the free memory)
     void set_hbm_budget(std::uint64_t bytes) { detail::check(ltg_set_hbm_budget(ctx_, bytes), ""); }
 
+    // device timing events of the calls (on by default; off for latency-bound loops)
+    void set_timing(bool on) { detail::check(ltg_set_timing(ctx_, on ? 1 : 0), ""); }
+
     // Multi-GPU: rank r of `world` processes (one GPU each) sharing `id`
     // (from nccl_unique_id() on rank 0, broadcast by the caller).
     void attach_nccl(const unsigned char id[128], int rank, int world) {

@@ -22,6 +22,7 @@
 // paths (recompute mode) and evaluates the same epilogue on the fly.
 #include <cuda_runtime.h>
 
+#include "finish.cuh"
 #include "kernels.h"
 #include "launch_config.h"
 #include "rng.cuh"
@@ -108,7 +109,11 @@ __device__ inline void bload(const BasketArgs& a, const BSmem& s, uint32_t width
 
 __device__ inline uint64_t bnext_chunk(const Work& w, uint32_t* slot) {
     __syncthreads();
-    if (threadIdx.x == 0) *slot = atomicAdd(w.counter, 1u);
+    if (threadIdx.x == 0) {  // (self-resetting counter: heston.cu next_chunk)
+        const uint32_t t = atomicAdd(w.counter, 1u);
+        if ((uint64_t)t == w.n_chunks + gridDim.x - 1) atomicExch(w.counter, 0u);
+        *slot = t;
+    }
     __syncthreads();
     return *slot;
 }
@@ -257,6 +262,7 @@ __global__ void __launch_bounds__(kBlock, 4) basket_pass1_kernel(BasketArgs a, W
             });
         }
     }
+    if (w.fuse) fused_tail(a.partials, w.n_chunks, width, w);
 }
 
 // sigmā contribution of instrument `pos` observed at maturity ms
@@ -323,6 +329,7 @@ __global__ void __launch_bounds__(kBlock, 4) basket_pass2_kernel(BasketArgs a, W
         double* row = a.partials + ci * width;
         bflush(s.acc, width, row, [](uint32_t t) { return t; });
     }
+    if (w.fuse) fused_tail(a.partials, w.n_chunks, width, w);
 }
 
 template <typename K>

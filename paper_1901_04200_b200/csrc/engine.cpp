@@ -368,6 +368,10 @@ struct ltg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[8] = {};
+    // ev_at[i]: the event that marks timing point i of the last call — its own,
+    // or an earlier one recorded at the same point of the stream (same_event),
+    // so a replayed graph carries no back-to-back event nodes
+    int ev_at[8] = {0, 1, 2, 3, 4, 5, 6, 7};
     std::string err;
     std::string rng_note;
 
@@ -376,6 +380,15 @@ struct ltg_ctx {
     double s0 = 0, mu = 0, dt = 0;
     std::vector<double> x0;
     std::vector<double> h_x;  // parameters of the current call
+    // [x | targets] on the device (d_x) when they do not fit the kernels'
+    // by-value arguments (upload_x), else null
+    const double* x_src = nullptr;
+    std::vector<double> h_t;  // targets of the current call (empty: none)
+    // lean calls: the host buffer the call's last reduction publishes the
+    // report into (Finish::pub), null otherwise; flag_clean: the rare flag is
+    // known to be zero (the last lean call's final kernel cleared it)
+    double* pub = nullptr;
+    bool flag_clean = true;
     std::vector<MaturityEvent> events;
     std::vector<uint32_t> inst_order;
 
@@ -415,8 +428,8 @@ struct ltg_ctx {
     // multi-GPU
     int rank = 0, world = 1;
     ncclComm_t comm = nullptr;
-    uint32_t fresh_slots = 0;  // scheduler slots zeroed by this call's flag memset, not yet used
     int timing_pending = 0;    // 1 / 2: `timing`'s device times still to read (settle_timing)
+    bool timing_on = true;     // ltg_set_timing
 
     ltg_timing timing{};
 
@@ -458,7 +471,6 @@ void alloc_call_block(ltg_ctx* c) {
 template <typename Fn>
 int guarded(ltg_ctx* ctx, Fn&& fn) {
     try {
-        if (ctx) ctx->fresh_slots = 0;
         if (ctx && ctx->ready) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         fn();
         return LTG_OK;
@@ -471,8 +483,18 @@ int guarded(ltg_ctx* ctx, Fn&& fn) {
     }
 }
 
-void require(bool ok, const std::string& msg) {
+// validation: a literal message costs nothing on success; composed messages
+// go through require_f, which builds them only on failure (a small call's
+// host path runs a dozen checks)
+void require(bool ok, const char* msg) {
     if (!ok) throw Failure(LTG_EINVAL, msg);
+}
+void require(bool ok, const std::string& msg) {  // (context creation)
+    if (!ok) throw Failure(LTG_EINVAL, msg);
+}
+template <typename Msg>
+void require_f(bool ok, Msg&& msg) {
+    if (!ok) throw Failure(LTG_EINVAL, msg());
 }
 
 bool is_group(const ltg_ctx* c) { return c && !c->members.empty(); }
@@ -482,6 +504,30 @@ bool is_group(const ltg_ctx* c) { return c && !c->members.empty(); }
 // the context), and report the first failure. Validation failures happen identically on every member before any
 // collective, so a bad argument cannot leave some members waiting.
 void settle_timing(ltg_ctx* c);
+void set_pub(ltg_ctx* c, Finish& fin);
+void set_targets(ltg_ctx* c, Finish& fin);
+
+// Work::fuse: the launch's last CTA reduces its chunk table and finishes the
+// call (finish.cuh fused_tail) instead of launch_reduce_chunks — for tables
+// small enough that one CTA's (group, column) items cover them in at most
+// two rounds, and only on one GPU without a collective (its rows need no
+// all-gather first). LTG_FUSE_REDUCE=0 turns it off (tests: both forms).
+bool fuse_reduce(ltg_ctx* c, Work& w, uint32_t width, double* tot, const Finish& fin) {
+    static const bool on = [] {
+        const char* e = std::getenv("LTG_FUSE_REDUCE");
+        return !(e && e[0] == '0');
+    }();
+    const uint64_t ng = (w.n_chunks + kGroup - 1) / kGroup;
+    if (!on || c->world != 1 || c->comm || c->loop || w.n_chunks == 0 || w.chunk_begin != 0 ||
+        ng * width > 2 * uint64_t(kBlock))
+        return false;
+    w.fuse = 1;
+    w.done = counter_ptr(c, 3);
+    w.groups = c->d_groups.as<double>();
+    w.tot = tot;
+    w.fin = fin;
+    return true;
+}
 
 template <typename Fn>
 int group_run(ltg_ctx* g, Fn&& fn) {
@@ -675,7 +721,12 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
     a.sc.sqdt = a.sqdt;
     a.sc.mu_dt = a.mu_dt;
     a.sc.half_dt = a.half_dt;
-    a.x = c->d_x.as<double>();
+    a.x = c->x_src;
+    a.v0 = x[4];
+    if (c->nlev <= (uint32_t)kInlineLev) {
+        a.lev_inline = 1;
+        std::copy(x + 5, x + 5 + c->nlev, a.lev_in);
+    }
     a.s_nodes = c->d_snodes.as<double>();
     a.row_off = c->d_rowoff.as<uint16_t>();
     a.events = c->d_events.as<MaturityEvent>();
@@ -762,27 +813,23 @@ void enq_copy(ltg_ctx* c, void* dst, const void* src, size_t n, cudaMemcpyKind k
     cuda_check(cudaMemcpyAsync(dst, src, n, kind, c->stream), "copy");
 }
 void rec_event(ltg_ctx* c, int i) {
+    c->ev_at[i] = i;
+    if (!c->timing_on) return;  // (ltg_set_timing: no events; the device times read 0)
     if (t_rec && !t_rec->op(16, c->ev[i], nullptr, 0)) return;
     // (inside a capture: an event-record node, so the timing events work on replay)
     cuda_check(t_rec ? cudaEventRecordWithFlags(c->ev[i], c->stream, cudaEventRecordExternal)
                      : cudaEventRecord(c->ev[i], c->stream),
                "event");
 }
-
-// a scheduler slot before its launch: already zero if the call's flag
-// memset (reset_flags) cleared it and no launch has used it since
-void zero_counter(ltg_ctx* c, int slot) {
-    if (c->fresh_slots & (1u << slot)) {
-        c->fresh_slots &= ~(1u << slot);
-        return;
-    }
-    enq_memset(c, counter_ptr(c, slot), sizeof(uint32_t));
-}
+// timing point i is where point j was recorded (nothing enqueued between)
+void same_event(ltg_ctx* c, int i, int j) { c->ev_at[i] = c->ev_at[j]; }
 
 void validate_cfg(ltg_ctx* c, const ltg_mc_config* cfg, size_t M) {
     require(cfg != nullptr, "null MCConfig");
-    require(M == c->M, "parameter vector has " + std::to_string(M) + " entries, program has " +
-                           std::to_string(c->M));
+    require_f(M == c->M, [&] {
+        return "parameter vector has " + std::to_string(M) + " entries, program has " +
+               std::to_string(c->M);
+    });
     require(cfg->paths > 0, "forward_pass: paths must be > 0");
     require(cfg->precision == LTG_FP64 || cfg->precision == LTG_FP32, "unknown precision");
     require(cfg->precision == LTG_FP64 || c->kind == 0,
@@ -806,7 +853,7 @@ void check_params(ltg_ctx* c, const double* x) {
 // into d_res = [G, means, se, lambda]. Returns whether pass-2 checkpoints of the
 // step-1 path set were written.
 bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool targets,
-               bool want_ckpt) {
+               bool want_ckpt, bool last = false) {
     const uint64_t per = chunks_per_rank(plan, c->world);
     const uint64_t table_rows = per * c->world;
     const uint32_t width = 2 * c->m;
@@ -815,6 +862,14 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     c->d_tot1.ensure(width * 8);
 
     Work w = base_work(c, cfg, plan);
+    Finish fin{};
+    fin.means = 1;
+    fin.m = c->m;
+    fin.paths = cfg.paths;
+    if (targets) set_targets(c, fin);
+    fin.res = res_ptr(c);
+    if (last) set_pub(c, fin);  // (estimate_means: pass 1 ends the call)
+    const bool fused = fuse_reduce(c, w, width, c->d_tot1.as<double>(), fin);
     if (c->kind == 1) {
         // basket: (S, W) at every maturity for pass 2 (store mode) when it fits
         BasketArgs b = basket_args(c, c->h_x.data());
@@ -833,7 +888,6 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         b.store_stride = w.ckpt_stride;
         b.write_sums = 1;
         b.write_store = c->store_ok ? 1 : 0;
-        zero_counter(c, 0);
         rec_event(c, 0);
         if (w.n_chunks) cuda_check(launch_basket_pass1(b, w, 0, c->stream), "basket pass 1");
         rec_event(c, 1);
@@ -929,7 +983,6 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         a.z_chunks = c->z_chunks;
         a.z_stride = std::max<uint64_t>(1, c->z_chunks * plan.chunk_paths);
         a.write_z = c->z_chunks > 0 ? 1 : 0;
-        zero_counter(c, 0);
         rec_event(c, 0);
         if (w.n_chunks) cuda_check(launch_heston_pass1(a, w, 0, c->stream), "heston pass 1");
         rec_event(c, 1);
@@ -937,19 +990,17 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     } else {
         ckpt = c->store_ok;
     }
-    all_gather_rows(c, c->d_part1.as<double>(), per, width);
-    Finish fin{};
-    fin.means = 1;
-    fin.m = c->m;
-    fin.paths = cfg.paths;
-    fin.targets = targets ? c->d_x.as<double>() + c->M : nullptr;
-    fin.res = res_ptr(c);
-    cuda_check(launch_reduce_chunks(c->d_part1.as<double>(), plan.n_chunks, width,
-                                    c->d_groups.as<double>(), c->d_tot1.as<double>(), fin,
-                                    c->stream),
-               "reduce");
-    rec_event(c, 2);
-    c->timing.launches += reduce_launch_count(plan.n_chunks);
+    if (!fused) {
+        all_gather_rows(c, c->d_part1.as<double>(), per, width);
+        cuda_check(launch_reduce_chunks(c->d_part1.as<double>(), plan.n_chunks, width,
+                                        c->d_groups.as<double>(), c->d_tot1.as<double>(), fin,
+                                        c->stream),
+                   "reduce");
+        c->timing.launches += reduce_launch_count(plan.n_chunks);
+        rec_event(c, 2);
+    } else {
+        same_event(c, 2, 1);
+    }
     c->timing.paths_pass1 = plan.path_end - plan.path_begin;
     if (ckpt && c->kind == 0) {
         c->timing.seg_steps = c->seg_steps;
@@ -961,7 +1012,9 @@ bool run_pass1(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     return ckpt;
 }
 
-void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool have_ckpt) {
+// chained: enqueued right behind run_pass1 (its last timing point is pass 2's start)
+void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool have_ckpt,
+               bool chained = false) {
     const uint64_t per = chunks_per_rank(plan, c->world);
     const uint64_t table_rows = per * c->world;
     c->d_part2.ensure(table_rows * c->M * 8);
@@ -979,8 +1032,18 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
     a.draws = p2_draws;
     a.draws_row0 = p2_row0;
     Work w = base_work(c, cfg, plan);
+    Finish fin{};
+    fin.grad = 1;
+    fin.M = (uint32_t)c->M;
+    fin.paths = cfg.paths;
+    fin.grad_out = grad_ptr(c);
+    set_pub(c, fin);
+    bool fused = false;
     const uint32_t nseg = (c->steps + c->seg_steps - 1) / c->seg_steps;
-    rec_event(c, 3);
+    if (chained)
+        same_event(c, 3, 2);
+    else
+        rec_event(c, 3);
     if (w.n_chunks && c->kind == 1) {
         BasketArgs b = basket_args(c, c->h_x.data());
         b.lambda = res_ptr(c) + 1 + 2 * c->m;
@@ -991,8 +1054,8 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
         b.store = b.use_store ? c->d_ckpt.as<double2>() : nullptr;
         b.store_stride = w.ckpt_stride;
         if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
-        zero_counter(c, 2);
         w.counter = counter_ptr(c, 2);
+        fused = fuse_reduce(c, w, c->M, c->d_tot2.as<double>(), fin);
         cuda_check(launch_basket_pass2(b, w, 0, c->stream), "basket pass 2");
         c->timing.launches += 1;
     } else if (w.n_chunks) {
@@ -1029,14 +1092,12 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                 // no forward has range-checked the fresh path set
                 r.check_all = (sf || cfg.fresh_step2_paths) ? 1 : 0;
                 if (cfg.fresh_step2_paths) r.rare_thr = fresh_check_thr();
-                zero_counter(c, 1);
                 ww.counter = counter_ptr(c, 1);
                 cuda_check(launch_heston_pass1(r, ww, 0, c->stream), "heston replay");
                 HestonArgs b = a;
                 b.ckpt = c->d_ckpt.p;
                 b.smat = c->d_ckpt.as<char>() + smat_off;
                 b.partials = c->d_part2.as<double>() + ww.chunk_begin * c->M;
-                zero_counter(c, 2);
                 ww.counter = counter_ptr(c, 2);
                 cuda_check(launch_heston_pass2(b, ww, 0, c->stream), "heston pass 2");
                 c->timing.launches += 2;
@@ -1054,7 +1115,6 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
                     r.partials = nullptr;
                     r.check_all = 1;
                     r.rare_thr = fresh_check_thr();
-                    zero_counter(c, 1);
                     Work ww = w;
                     ww.counter = counter_ptr(c, 1);
                     cuda_check(launch_heston_pass1(r, ww, 0, c->stream), "heston range check");
@@ -1068,25 +1128,24 @@ void run_pass2(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bool
             a.z_stride = std::max<uint64_t>(1, c->z_chunks * plan.chunk_paths);
             a.use_z = (c->z_chunks > 0 && !cfg.fresh_step2_paths) ? 1 : 0;
             a.partials = c->d_part2.as<double>() + plan.chunk_begin * c->M;
-            zero_counter(c, 2);
             w.counter = counter_ptr(c, 2);
+            fused = fuse_reduce(c, w, c->M, c->d_tot2.as<double>(), fin);
             cuda_check(launch_heston_pass2(a, w, 0, c->stream), "heston pass 2");
             c->timing.launches += 1;
         }
     }
     rec_event(c, 4);
-    all_gather_rows(c, c->d_part2.as<double>(), per, c->M);
-    Finish fin{};
-    fin.grad = 1;
-    fin.M = (uint32_t)c->M;
-    fin.paths = cfg.paths;
-    fin.grad_out = grad_ptr(c);
-    cuda_check(launch_reduce_chunks(c->d_part2.as<double>(), plan.n_chunks, c->M,
-                                    c->d_groups.as<double>(), c->d_tot2.as<double>(), fin,
-                                    c->stream),
-               "reduce");
-    rec_event(c, 5);
-    c->timing.launches += reduce_launch_count(plan.n_chunks);
+    if (!fused) {
+        all_gather_rows(c, c->d_part2.as<double>(), per, c->M);
+        cuda_check(launch_reduce_chunks(c->d_part2.as<double>(), plan.n_chunks, c->M,
+                                        c->d_groups.as<double>(), c->d_tot2.as<double>(), fin,
+                                        c->stream),
+                   "reduce");
+        c->timing.launches += reduce_launch_count(plan.n_chunks);
+        rec_event(c, 5);
+    } else {
+        same_event(c, 5, 4);
+    }
     c->timing.paths_pass2 = plan.path_end - plan.path_begin;
 }
 
@@ -1106,14 +1165,8 @@ void run_tangent(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bo
     a.write_sums = sums ? 1 : 0;
     Work w = base_work(c, cfg, plan);
     if (cfg.fresh_step2_paths) w.path_offset += cfg.paths;
-    zero_counter(c, 2);
     w.counter = counter_ptr(c, 2);
-    rec_event(c, sums ? 0 : 3);
-    if (w.n_chunks) cuda_check(launch_heston_tangent(a, w, 0, c->stream), "heston tangent");
-    rec_event(c, sums ? 1 : 4);
-    c->timing.launches += w.n_chunks ? 1 : 0;
-    all_gather_rows(c, c->d_part2.as<double>(), per, width);
-    // one finishing launch: (means, lambda, G when this launch is pass 1) then
+    // one finishing step: (means, lambda, G when this launch is pass 1) then
     // grad = sum_i lambda_i J_i / P
     Finish fin{};
     fin.means = sums ? 1 : 0;
@@ -1121,21 +1174,32 @@ void run_tangent(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan, bo
     fin.m = c->m;
     fin.M = (uint32_t)c->M;
     fin.paths = cfg.paths;
-    fin.targets = c->d_x.as<double>() + c->M;
+    set_targets(c, fin);
     fin.res = res_ptr(c);
     fin.grad_out = grad_ptr(c);
-    cuda_check(launch_reduce_chunks(c->d_part2.as<double>(), plan.n_chunks, width,
-                                    c->d_groups.as<double>(), c->d_tot2.as<double>(), fin,
-                                    c->stream),
-               "reduce");
-    c->timing.launches += reduce_launch_count(plan.n_chunks);
-    if (sums) {
-        c->timing.paths_pass1 = plan.path_end - plan.path_begin;
-        rec_event(c, 2);
-        rec_event(c, 3);
-        rec_event(c, 4);
+    set_pub(c, fin);
+    const bool fused = fuse_reduce(c, w, width, c->d_tot2.as<double>(), fin);
+    rec_event(c, sums ? 0 : 3);
+    if (w.n_chunks) cuda_check(launch_heston_tangent(a, w, 0, c->stream), "heston tangent");
+    rec_event(c, sums ? 1 : 4);
+    c->timing.launches += w.n_chunks ? 1 : 0;
+    if (!fused) {
+        all_gather_rows(c, c->d_part2.as<double>(), per, width);
+        cuda_check(launch_reduce_chunks(c->d_part2.as<double>(), plan.n_chunks, width,
+                                        c->d_groups.as<double>(), c->d_tot2.as<double>(), fin,
+                                        c->stream),
+                   "reduce");
+        c->timing.launches += reduce_launch_count(plan.n_chunks);
+        rec_event(c, 5);
+    } else {
+        same_event(c, 5, sums ? 1 : 4);
     }
-    rec_event(c, 5);
+    if (sums) {  // (pass 1 and the gradient in one launch: no pass-2 span)
+        c->timing.paths_pass1 = plan.path_end - plan.path_begin;
+        same_event(c, 2, 5);
+        same_event(c, 3, 5);
+        same_event(c, 4, 5);
+    }
     c->timing.paths_pass2 = plan.path_end - plan.path_begin;
 }
 
@@ -1149,15 +1213,17 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 // (ltg_last_timing) rather than inside the call: seven event queries cost
 // more than the whole host side of a replayed small call.
 void settle_timing(ltg_ctx* c) {
+    auto E = [c](int i) { return c->ev[c->ev_at[i]]; };
+    if (!c->timing_on) c->timing_pending = 0;
     if (c->timing_pending == 1) {  // gradient_of_G: pass 1, pass 2, both reductions
-        c->timing.pass1_ms = elapsed(c->ev[0], c->ev[1]);
-        c->timing.pass2_ms = elapsed(c->ev[3], c->ev[4]);
-        c->timing.reduce_ms = elapsed(c->ev[1], c->ev[2]) + elapsed(c->ev[4], c->ev[5]);
-        c->timing.total_ms = elapsed(c->ev[0], c->ev[5]);
+        c->timing.pass1_ms = elapsed(E(0), E(1));
+        c->timing.pass2_ms = elapsed(E(3), E(4));
+        c->timing.reduce_ms = elapsed(E(1), E(2)) + elapsed(E(4), E(5));
+        c->timing.total_ms = elapsed(E(0), E(5));
     } else if (c->timing_pending == 2) {  // estimate_means: pass 1 and its reduction
-        c->timing.pass1_ms = elapsed(c->ev[0], c->ev[1]);
-        c->timing.reduce_ms = elapsed(c->ev[1], c->ev[2]);
-        c->timing.total_ms = elapsed(c->ev[0], c->ev[2]);
+        c->timing.pass1_ms = elapsed(E(0), E(1));
+        c->timing.reduce_ms = elapsed(E(1), E(2));
+        c->timing.total_ms = elapsed(E(0), E(2));
     }
     c->timing_pending = 0;
 }
@@ -1174,10 +1240,12 @@ int start_safe(const ltg_ctx* c) {
     return (e && e[0] == '1') || !c->h_rc.exact_exp ? 1 : 0;
 }
 
-// One memset at the start of a call: the rare flag and every scheduler slot.
+// One memset at the start of a call: the rare flag (and the scheduler slots,
+// which their launches leave zero anyway). The call's kernels may set the
+// flag again; only a lean call's last kernel clears it (flag_clean).
 void reset_flags(ltg_ctx* c) {
     enq_memset(c, flags_ptr(c), kFlagWords * 4);
-    c->fresh_slots = 0x7;
+    c->flag_clean = false;
 }
 
 // The rare flag after the call's kernels: all-reduced over the ranks (NCCL);
@@ -1217,14 +1285,49 @@ bool wait_rare(ltg_ctx* c, const double* host_slot) {
     return v != 0;
 }
 
+// The call's x and targets. The kernels take v0, the leverage cells and the
+// targets by value when they fit (HestonArgs::lev_in, Finish::tgt_in); only
+// larger models copy [x | targets] to d_x (one H2D copy from the pinned
+// staging area).
 void upload_x(ltg_ctx* c, const double* x, const double* targets) {
     c->h_x.assign(x, x + c->M);
+    if (targets)
+        c->h_t.assign(targets, targets + c->m);
+    else
+        c->h_t.clear();
+    const bool fits = (c->kind != 0 || c->nlev <= (uint32_t)kInlineLev) &&
+                      (!targets || c->m <= (uint32_t)kInlineTargets);
+    if (fits) {
+        c->x_src = nullptr;
+        return;
+    }
     const size_t n = c->M + (targets ? c->m : 0);
     double* st = c->stage(n);
     std::memcpy(st, x, c->M * 8);
     if (targets) std::memcpy(st + c->M, targets, c->m * 8);
     c->d_x.ensure((c->M + c->m) * 8);  // [x | targets]: one copy
     enq_copy(c, c->d_x.p, st, n * 8, cudaMemcpyHostToDevice);
+    c->x_src = c->d_x.as<double>();
+}
+
+// the targets of a finishing launch: by value, or behind x in d_x
+void set_targets(ltg_ctx* c, Finish& fin) {
+    if (c->h_t.empty()) return;
+    if (c->m <= (uint32_t)kInlineTargets) {
+        fin.tgt_inline = 1;
+        std::copy(c->h_t.begin(), c->h_t.end(), fin.tgt_in);
+    } else {
+        fin.targets = c->x_src + c->M;
+    }
+}
+
+// the report of a lean call (its last reduction publishes it, Finish::pub)
+void set_pub(ltg_ctx* c, Finish& fin) {
+    if (!c->pub) return;
+    fin.pub = c->pub;
+    fin.pub_src = res_ptr(c);
+    fin.pub_n = (uint32_t)out_doubles(c);
+    fin.rare = rare_ptr(c);
 }
 
 bool graphs_enabled() {
@@ -1595,15 +1698,17 @@ struct DrawScope {
         if (!src) return;
         require(src->data != nullptr, "null draw buffer");
         require(cfg.precision == LTG_FP64, "caller draws: fp64 only (the reference's arithmetic)");
-        require(src->dim == ctx->N, "forward_pass: draw source dimension " +
-                                        std::to_string(src->dim) + " != tape randoms " +
-                                        std::to_string(ctx->N));
+        require_f(src->dim == ctx->N, [&] {
+            return "forward_pass: draw source dimension " + std::to_string(src->dim) +
+                   " != tape randoms " + std::to_string(ctx->N);
+        });
         require(src->rows <= (uint64_t(1) << 62) / std::max<uint64_t>(1, src->dim),
                 "draw buffer size overflows");
         const uint64_t need_rows = cfg.fresh_step2_paths ? 2 * cfg.paths : cfg.paths;
-        require(src->rows >= need_rows,
-                "BufferDrawSource: path index out of range (" + std::to_string(need_rows) +
-                    " paths need draws, the buffer has " + std::to_string(src->rows) + ")");
+        require_f(src->rows >= need_rows, [&] {
+            return "BufferDrawSource: path index out of range (" + std::to_string(need_rows) +
+                   " paths need draws, the buffer has " + std::to_string(src->rows) + ")";
+        });
         c = ctx;
         const uint64_t rows = plan.path_end - plan.path_begin;
         const uint64_t n_regions = cfg.fresh_step2_paths ? 2 : 1;
@@ -1665,8 +1770,10 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
         validate_cfg(ctx, cfg, M);
         require(x && targets && report && report->means && report->lambda && report->grad,
                 "null buffer");
-        require(m == ctx->m, "gradient_of_G: " + std::to_string(m) + " targets for " +
-                                 std::to_string(ctx->m) + " outputs");
+        require_f(m == ctx->m, [&] {
+            return "gradient_of_G: " + std::to_string(m) + " targets for " +
+                   std::to_string(ctx->m) + " outputs";
+        });
         require(!(cfg->memory_mode == LTG_MODE_STORE && cfg->fresh_step2_paths),
                 "gradient_of_G: fresh_step2_paths replays nothing, so stored forward state "
                 "cannot be used; switch to recompute mode");
@@ -1689,11 +1796,22 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
                     "fp32 gradient_of_G needs the Feller condition 2*kappa*theta >= xi^2 "
                     "(its accuracy bar is not met at the variance truncation kink); use fp64");
         const uint32_t nm = ctx->m;
-        // one pinned staging area per call: x and the targets in, the report
+        // one pinned staging area per call: [x | targets] in, then the report
         // and the rare flag out (sized up front: a graph captures its address)
-        double* st = ctx->stage(std::max<size_t>(ctx->M + nm, out_doubles(ctx) + 1));
-        const bool graphable = !src && !ctx->comm && !ctx->loop && ctx->world == 1 &&
-                               !cfg->fresh_step2_paths;
+        const size_t base = ctx->M + nm;
+        double* st = ctx->stage(base + out_doubles(ctx) + 1);
+        double* out = st + base;
+        // lean call (one GPU, no collective): the kernels read [x | targets]
+        // from the staging area, the last reduction writes the report back
+        // into it and clears the rare flag, so the call's device work is its
+        // kernels alone — no H2D / D2H copy, no flag memset
+        const bool lean = !src && !ctx->comm && !ctx->loop && ctx->world == 1;
+        const bool graphable = lean && !cfg->fresh_step2_paths;
+        struct PubScope {
+            ltg_ctx* c;
+            ~PubScope() { c->pub = nullptr; }
+        } pub_scope{ctx};
+        ctx->pub = lean ? out : nullptr;
         const std::string key = std::string(tangent ? "tangent" : "grad") + "/" +
                                 std::to_string(cfg->paths) + "/" + std::to_string(cfg->antithetic) +
                                 "/" + std::to_string(cfg->precision);
@@ -1705,7 +1823,7 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
             ctx->timing.safe_rerun = rerun;
             run_body(ctx, graphable && !ctx->safe, key, [&] {
                 upload_x(ctx, x, targets);
-                reset_flags(ctx);
+                if (!lean || !ctx->flag_clean) reset_flags(ctx);
                 if (tangent) {
                     if (cfg->fresh_step2_paths) {
                         run_pass1(ctx, *cfg, plan, true, false);
@@ -1715,19 +1833,21 @@ int gradient_impl(ltg_ctx* ctx, const double* x, size_t M, const double* targets
                     }
                 } else {
                     const bool ckpt = run_pass1(ctx, *cfg, plan, true, !cfg->fresh_step2_paths);
-                    run_pass2(ctx, *cfg, plan, ckpt);
+                    run_pass2(ctx, *cfg, plan, ckpt, true);
                 }
-                copy_out(ctx, st);
+                if (!lean) copy_out(ctx, out);
             });
-            if (!wait_rare(ctx, st + out_doubles(ctx)) || ctx->safe) break;
+            const bool rare = wait_rare(ctx, out + out_doubles(ctx));
+            if (lean) ctx->flag_clean = true;  // (the last reduction cleared it)
+            if (!rare || ctx->safe) break;
         }
         ctx->safe = 0;
         ctx->timing_pending = 1;  // event times read on demand (settle_timing)
-        report->G = st[0];
-        std::memcpy(report->means, st + 1, nm * 8);
-        if (report->std_errors) std::memcpy(report->std_errors, st + 1 + nm, nm * 8);
-        std::memcpy(report->lambda, st + 1 + 2 * nm, nm * 8);
-        std::memcpy(report->grad, st + 1 + 3 * nm, ctx->M * 8);
+        report->G = out[0];
+        std::memcpy(report->means, out + 1, nm * 8);
+        if (report->std_errors) std::memcpy(report->std_errors, out + 1 + nm, nm * 8);
+        std::memcpy(report->lambda, out + 1 + 2 * nm, nm * 8);
+        std::memcpy(report->grad, out + 1 + 3 * nm, ctx->M * 8);
         report->paths = cfg->paths;
         report->seed = cfg->seed;
         report->mode = cfg->memory_mode;
@@ -1829,8 +1949,17 @@ int means_impl(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg
         const ltg_shard plan = make_plan(cfg->paths, ctx->rank, ctx->world);
         const DrawScope draws(ctx, src, *cfg, plan);
         const uint32_t nm = ctx->m;
-        double* st = ctx->stage(std::max<size_t>(ctx->M, out_doubles(ctx) + 1));
-        const bool graphable = !src && !ctx->comm && !ctx->loop && ctx->world == 1;
+        // staging: [x] in, the report and the rare flag out (as gradient_impl)
+        const size_t base = ctx->M;
+        double* st = ctx->stage(base + out_doubles(ctx) + 1);
+        double* out = st + base;
+        const bool lean = !src && !ctx->comm && !ctx->loop && ctx->world == 1;
+        const bool graphable = lean;
+        struct PubScope {
+            ltg_ctx* c;
+            ~PubScope() { c->pub = nullptr; }
+        } pub_scope{ctx};
+        ctx->pub = lean ? out : nullptr;
         const std::string key = "means/" + std::to_string(cfg->paths) + "/" +
                                 std::to_string(cfg->antithetic) + "/" +
                                 std::to_string(cfg->precision);
@@ -1842,16 +1971,18 @@ int means_impl(ltg_ctx* ctx, const double* x, size_t M, const ltg_mc_config* cfg
             ctx->timing.safe_rerun = rerun;
             run_body(ctx, graphable && !ctx->safe, key, [&] {
                 upload_x(ctx, x, nullptr);
-                reset_flags(ctx);
-                run_pass1(ctx, *cfg, plan, false, false);
-                copy_out(ctx, st);
+                if (!lean || !ctx->flag_clean) reset_flags(ctx);
+                run_pass1(ctx, *cfg, plan, false, false, true);
+                if (!lean) copy_out(ctx, out);
             });
-            if (!wait_rare(ctx, st + out_doubles(ctx)) || ctx->safe) break;
+            const bool rare = wait_rare(ctx, out + out_doubles(ctx));
+            if (lean) ctx->flag_clean = true;
+            if (!rare || ctx->safe) break;
         }
         ctx->safe = 0;
         ctx->timing_pending = 2;
-        std::memcpy(means, st + 1, nm * 8);
-        if (std_errors) std::memcpy(std_errors, st + 1 + nm, nm * 8);
+        std::memcpy(means, out + 1, nm * 8);
+        if (std_errors) std::memcpy(std_errors, out + 1 + nm, nm * 8);
     });
 }
 
@@ -1988,7 +2119,6 @@ int ltg_path_payoffs(ltg_ctx* ctx, const double* x, size_t M, uint64_t seed, int
         ctx->seg_steps = 16;
         ctx->d_part1.ensure(plan.n_chunks * 2 * ctx->m * 8);
         ctx->d_normals.ensure(npaths * ctx->m * 8);
-        zero_counter(ctx, 0);
         if (ctx->kind == 0) {
             ctx->fp32 = 0;
             HestonArgs a = heston_args(ctx, ctx->h_x.data());
@@ -2016,6 +2146,13 @@ int ltg_set_hbm_budget(ltg_ctx* ctx, uint64_t bytes) {
     if (!ctx) return LTG_EINVAL;
     ctx->hbm_budget = bytes;
     for (auto& m : ctx->members) m->hbm_budget = bytes;
+    return LTG_OK;
+}
+
+int ltg_set_timing(ltg_ctx* ctx, int on) {
+    if (!ctx) return LTG_EINVAL;
+    ctx->timing_on = on != 0;
+    for (auto& mb : ctx->members) mb->timing_on = on != 0;
     return LTG_OK;
 }
 

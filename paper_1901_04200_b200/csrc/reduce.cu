@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.h"
+#include "finish.cuh"
 #include "rng.cuh"
 
 namespace ltg {
@@ -51,63 +52,6 @@ __global__ void __launch_bounds__(kFinishThreads) reduce_groups_kernel(
     const uint64_t c0 = g * kGroup;
     const uint64_t c1 = min(c0 + (uint64_t)kGroup, n_chunks);
     ordered_column_sums(table, c0, c1, width, groups + g * width, tile);
-}
-
-// means_from_sums (expectation.hpp:251-269) for output o
-__device__ void finalize_mean(const double* totals, uint32_t m, uint64_t paths,
-                              const double* targets, double* res, uint32_t o) {
-    const double P = (double)paths;
-    const double mean = __ddiv_rn(totals[o], P);
-    res[1 + o] = mean;
-    if (paths > 1) {
-        double var = __ddiv_rn(__dsub_rn(totals[m + o], __dmul_rn(__dmul_rn(P, mean), mean)),
-                               __dsub_rn(P, 1.0));
-        var = var > 0.0 ? var : 0.0;
-        res[1 + m + o] = __dsqrt_rn(__ddiv_rn(var, P));
-    } else {
-        res[1 + m + o] = 0.0;
-    }
-    if (targets) res[1 + 2 * m + o] = __dsub_rn(mean, targets[o]);  // lambda (:329-334)
-}
-
-// Group sums -> totals (ascending group order), then the call's finishing
-// step in the same single-CTA launch:
-//   means: means, std errors, lambda per output (one thread each), then
-//          G = sum_o 0.5 * lambda_o^2 in ascending o (:329-334);
-//   grad:  grad = total / P (:340-342);
-//   grad_tangent: grad[d] = (sum_i lambda_i * J[i][d]) / P, i ascending,
-//          J = totals + 2m, lambda from res (written by `means` above when
-//          both are set).
-__device__ void finish_call(const double* out, const Finish& f) {
-    if (!(f.means || f.grad || f.grad_tangent)) return;
-    __syncthreads();  // out visible to the block
-    if (f.means) {
-        for (uint32_t o = threadIdx.x; o < f.m; o += blockDim.x)
-            finalize_mean(out, f.m, f.paths, f.targets, f.res, o);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double G = 0.0;
-            if (f.targets) {
-                const double* lambda = f.res + 1 + 2 * f.m;
-                for (uint32_t o = 0; o < f.m; ++o)
-                    G = __dadd_rn(G, __dmul_rn(__dmul_rn(0.5, lambda[o]), lambda[o]));
-            }
-            f.res[0] = G;
-        }
-    }
-    if (f.grad)
-        for (uint32_t j = threadIdx.x; j < f.M; j += blockDim.x)
-            f.grad_out[j] = __ddiv_rn(out[j], (double)f.paths);
-    if (f.grad_tangent) {
-        const double* J = out + 2 * f.m;
-        const double* lambda = f.res + 1 + 2 * f.m;
-        for (uint32_t d = threadIdx.x; d < f.M; d += blockDim.x) {
-            double t = 0.0;
-            for (uint32_t i = 0; i < f.m; ++i)
-                t = __dadd_rn(t, __dmul_rn(lambda[i], J[(size_t)i * f.M + d]));
-            f.grad_out[d] = __ddiv_rn(t, (double)f.paths);
-        }
-    }
 }
 
 __global__ void __launch_bounds__(kFinishThreads) reduce_final_kernel(

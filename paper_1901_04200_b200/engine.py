@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH):
                                  C.c_int, C.c_uint64, C.c_uint64, _dp, _dp, _dp]
     L.ltg_last_timing.argtypes = [C.c_void_p, C.POINTER(TimingC)]
     L.ltg_set_hbm_budget.argtypes = [C.c_void_p, C.c_uint64]
+    L.ltg_set_timing.argtypes = [C.c_void_p, C.c_int]
     L.ltg_path_payoffs.argtypes = [C.c_void_p, _dp, C.c_size_t, C.c_uint64, C.c_int, C.c_uint64,
                                    C.c_uint64, _dp]
     L.ltg_rng_exact.argtypes = [C.c_void_p]
@@ -354,6 +355,14 @@ class Engine:
     def set_hbm_budget(self, nbytes: int) -> None:
         """Cap the HBM held for checkpoints + draw store (0: free memory)."""
         rc = self.lib.ltg_set_hbm_budget(self.h, int(nbytes))
+        if rc:
+            self._raise(rc)
+
+    def set_timing(self, on: bool) -> None:
+        """Device timing events of the calls (ltg_set_timing; on by default):
+        off takes the events out of a small call's critical path, and
+        timing() then reports zero device times."""
+        rc = self.lib.ltg_set_timing(self.h, 1 if on else 0)
         if rc:
             self._raise(rc)
 
