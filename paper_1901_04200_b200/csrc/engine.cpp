@@ -511,15 +511,16 @@ void set_targets(ltg_ctx* c, Finish& fin);
 // call (finish.cuh fused_tail) instead of launch_reduce_chunks — for tables
 // small enough that one CTA's (group, column) items cover them in at most
 // two rounds, and only on one GPU without a collective (its rows need no
-// all-gather first). LTG_FUSE_REDUCE=0 turns it off (tests: both forms).
+// all-gather first), with the fast Philox kernels (a safe rerun or caller
+// draws reduce separately). LTG_FUSE_REDUCE=0 turns it off (tests: both forms).
 bool fuse_reduce(ltg_ctx* c, Work& w, uint32_t width, double* tot, const Finish& fin) {
     static const bool on = [] {
         const char* e = std::getenv("LTG_FUSE_REDUCE");
         return !(e && e[0] == '0');
     }();
     const uint64_t ng = (w.n_chunks + kGroup - 1) / kGroup;
-    if (!on || c->world != 1 || c->comm || c->loop || w.n_chunks == 0 || w.chunk_begin != 0 ||
-        ng * width > 2 * uint64_t(kBlock))
+    if (!on || c->world != 1 || c->comm || c->loop || c->safe || c->draws_on || w.n_chunks == 0 ||
+        w.chunk_begin != 0 || ng * width > 2 * uint64_t(kBlock))
         return false;
     w.fuse = 1;
     w.done = counter_ptr(c, 3);
