@@ -7,7 +7,7 @@ CFG5=0; [ "$1" = "--cfg5" ] && { CFG5=1; shift; }
 for v in main "$@"; do
   lib=""; [ "$v" != main ] && lib=paper_1901_04200_b200/_lib/variants/$v.so
   for rep in 1 2; do
-    env LTG_ZSTORE=0 ${lib:+LTG_LIB=$lib} timeout 200 python tools/quick_time.py cfg3 cfg3:fp32 cfg4 cfg2 2>&1 | python -c "
+    env LTG_ZSTORE=0 ${lib:+LTG_LIB=$lib} timeout 200 python tools/quick_time.py ${QT_CFGS:-cfg3 cfg3:fp32 cfg4 cfg2} 2>&1 | python -c "
 import sys, json
 for l in sys.stdin:
     try:
