@@ -39,6 +39,9 @@ int main(int argc, char** argv) {
         cfg.paths = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : spec.mc.paths;
         cfg.seed = spec.mc.seed;
         const std::vector<double> targets = engine.estimate_means(truth, cfg).means;
+        // a latency-bound loop of small calls: no timing events on the device
+        // (ltg_set_timing), each call is its kernels alone
+        engine.set_timing(false);
 
         const auto g = gpu::make_objective<lt::GradientReport>(engine, targets, cfg);
         // count the evaluations the calibrator makes (one gradient_of_G per
