@@ -80,18 +80,8 @@ __device__ inline void finish_call(const double* out, const Finish& f) {
 // order, every sum starting from 0.0 — and finishes the call. Thread items
 // are (group, column) pairs, so the groups' addition chains run in parallel.
 // Called by all threads of every CTA after its last chunk row is written.
-#ifndef LTG_TAIL_NOINLINE
-#define LTG_TAIL_NOINLINE 0
-#endif
-#if LTG_TAIL_NOINLINE
-static __device__ __noinline__
-#else
-__device__ inline
-#endif
-void fused_tail(const double* table, uint64_t n_chunks, uint32_t width, const Work& w) {
-#ifdef LTG_NO_FUSED_TAIL
-    return;
-#endif
+__device__ inline void fused_tail(const double* table, uint64_t n_chunks, uint32_t width,
+                                  const Work& w) {
     __shared__ uint32_t is_last;
     __threadfence();  // every thread's row writes before the CTA's count
     __syncthreads();

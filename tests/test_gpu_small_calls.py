@@ -98,3 +98,32 @@ def test_rare_flag_does_not_leak_into_the_next_call():
         m = eng.estimate_means(c.x, cfg)
         assert eng.timing()["safe_rerun"] == 0
         assert m.means == ref.estimate_means(c.x, cfg).means
+
+
+@pytest.mark.parametrize("m,rows,cols,paths", [(64, 4, 8, 3000), (65, 4, 8, 3000),
+                                               (80, 6, 6, 2500), (80, 6, 6, 1 << 17)])
+def test_models_beyond_the_by_value_arguments(ref, golden_dir, m, rows, cols, paths):
+    # up to 32 leverage cells and 64 targets travel in the launch arguments;
+    # larger models take the one-copy route through d_x — both against the
+    # reference, with the fused (small) and the separate (2^17) reduction
+    import copy
+    from paper_1901_04200_b200.model import CALL, PUT, Instrument, load_model_spec
+    from test_gpu_parity import assert_report_close
+    spec = copy.deepcopy(load_model_spec(os.path.join(golden_dir, "heston_small.json")))
+    g = np.random.default_rng(m * 1000 + rows)
+    steps = spec.mc.steps
+    spec.grid.t_nodes = [i * steps * spec.mc.dt / rows for i in range(rows)]
+    spec.grid.s_nodes = [float(v) for v in np.linspace(70.0, 130.0, cols)]
+    spec.grid.values = [float(v) for v in g.uniform(0.6, 1.4, rows * cols)]
+    spec.instruments = [Instrument(int(g.choice([CALL, PUT])), float(g.uniform(80.0, 120.0)),
+                                   int(g.integers(1, steps + 1))) for _ in range(m)]
+    eng = Engine(spec)
+    prog = ref.program(spec)
+    x = prog.initial_params()
+    assert len(x) == 5 + rows * cols
+    means, _ = prog.estimate_means(x, 4096, 77, workers=8)
+    targets = 0.95 * means
+    orc = prog.gradient_of_G(x, targets, paths, 11, workers=8)
+    for _ in range(3):  # eager, capture, replay
+        rep = eng.gradient_of_G(x, targets, MCConfig(paths=paths, seed=11))
+        assert_report_close(rep, orc)
