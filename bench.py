@@ -407,7 +407,7 @@ def main():
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
                 "basis": ("algorithmic: the kernels' executed " +
                           ("FADD+FMUL+FFMA" if fp32 else "DADD+DMUL+DFMA") +
-                          " per path (ncu census, profiles/r2_census.txt) minus the redundant "
+                          " per path (ncu census, profiles/r3_census.txt) minus the redundant "
                           "AS241 central-branch evaluations on tail slots; pass 2 weighted by "
                           "the draw-store share"),
                 "census_inst_per_path": {b: w[b] for b in w},
@@ -419,6 +419,16 @@ def main():
                                 "chains/thread, full occupancy)") if fp32 else
                                ("measured in this run: ltg_probe_fp64_rate (fastest of DFMA, "
                                 "DMUL+DADD, DADD streams; 8 chains/thread, full occupancy)")}
+        # cross-check against SURVEY.md §8(d)'s preliminary W (FP64 issues per
+        # path with its per-op weights; it credits both passes with drawing
+        # every normal, also where pass 2 reads the draw store)
+        w8d = census.survey_w(cfg.name) if not fp32 and args.method == "adjoint" else None
+        if w8d is not None:
+            roof["survey_8d"] = {
+                "W_per_path": w8d,
+                "whole_step_frac": w8d * paths_rank / t_step / peak,
+                "note": "SURVEY.md §8(d) preliminary W (not the census): an upper figure, "
+                        "the bench's frac stays the census"}
         trf = census.dram_per_path(cfg.name, prec, dom, zf)
         if trf is not None and args.method == "adjoint":
             # ncu DRAM bytes/path of the dominant kernel (with and without the

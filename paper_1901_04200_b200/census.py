@@ -117,3 +117,13 @@ def dram_per_path(name: str, precision: str, kernel: str, store_fraction: float 
     if kernel == "pass1":
         return (1.0 - store_fraction) * t["pass1"] + store_fraction * t["pass1_store"]
     return (1.0 - store_fraction) * t["pass2_regen"] + store_fraction * t["pass2_store"]
+
+
+# SURVEY.md §8(d)'s preliminary algorithmic work per path (FP64 issues with its
+# per-op weights, both passes drawing every normal): a cross-check figure
+# beside the census, reported by bench.py as roofline.survey_8d.
+SURVEY_W = {"cfg1_gbm": 2.4e3, "cfg2_localvol": 1.14e4, "cfg3_heston": 2.6e5, "cfg4_basket16": 1.33e5}
+
+
+def survey_w(name: str) -> Optional[float]:
+    return SURVEY_W.get(_key(name, "fp64")[0])
