@@ -59,7 +59,7 @@ DRAM: Dict[Tuple[str, str], Dict[str, float]] = {
 
 # central-batch widths and normal batches of the kernels (heston.cu: kPass1PB,
 # kPass2PB, kGenSteps; the checkpoint interval KS = 8 of every BASELINE plan)
-_PB = {("fp64", "pass1"): 16, ("fp32", "pass1"): 4, ("fp64", "pass2"): 16, ("fp32", "pass2"): 4}
+_PB = {("fp64", "pass1"): 16, ("fp32", "pass1"): 4, ("fp64", "pass2"): 16, ("fp32", "pass2"): 8}
 _BATCH_STEPS = 8
 
 

@@ -161,7 +161,7 @@ __device__ __forceinline__ void simulate(const BasketArgs& a, const BSmem& s, co
             copy_draws<double>(drow, valid, 2 * pair0, 2 * npairs, a.steps * n, zb);
         else
             gen_segment<BGS, LTG_BPB, (LTG_BASKET_FUSED != 0)>(base, neg, pair0, npairs,
-                                                               w.seed_lo, w.seed_hi, zb, wl,
+                                                               w.rk, zb, wl,
                                                                *s.tab, a.rc);
         for (uint32_t j = 0; j < nb; ++j) {
             const uint32_t k = k0 + j;

@@ -796,8 +796,7 @@ Work base_work(ltg_ctx* c, const ltg_mc_config& cfg, const ltg_shard& plan) {
     w.ckpt_path0 = plan.path_begin;
     w.ckpt_stride = std::max<uint64_t>(1, plan.path_end - plan.path_begin);
     w.counter = counter_ptr(c, 0);
-    w.seed_lo = (uint32_t)cfg.seed;
-    w.seed_hi = (uint32_t)(cfg.seed >> 32);
+    w.rk = make_philox_keys((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
     // (caller draws: no antithetic pairing, so the kernels' Philox path word
     // is the path index, which also addresses the caller's row)
     w.antithetic = cfg.antithetic && !c->draws_on ? 1 : 0;

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kFinishThreads) reduce_final_kernel(
 // generator (gen_segment), one path per thread.
 constexpr int KF = 16;
 __global__ void __launch_bounds__(kBlock) fill_normals_kernel(
-    const RngTables* tables, RngConsts rc, uint32_t seed_lo, uint32_t seed_hi, int antithetic,
+    const RngTables* tables, RngConsts rc, PhiloxKeys rk, int antithetic,
     uint64_t path0, uint64_t npaths, uint32_t dim, double* __restrict__ out) {
     __shared__ RngTables sh;
     __shared__ double zbuf[2 * KF * kBlock];
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kBlock) fill_normals_kernel(
     uint16_t* wl = wlist + (threadIdx.x >> 5) * 64 * KF;
     for (uint32_t k0 = 0; k0 < pairs; k0 += KF) {
         const int kn = (int)min((uint32_t)KF, pairs - k0);
-        gen_segment<KF>(base, neg, k0, kn, seed_lo, seed_hi, zb, wl, sh, rc);
+        gen_segment<KF>(base, neg, k0, kn, rk, zb, wl, sh, rc);
         if (i < npaths)
             for (int s = 0; s < 2 * kn; ++s) {
                 const uint32_t slot = 2 * k0 + s;
@@ -123,7 +123,7 @@ cudaError_t launch_fill_normals(const RngTables* tables, const RngConsts& rc, ui
                                 uint32_t dim, double* out, cudaStream_t s) {
     if (npaths == 0 || dim == 0) return cudaSuccess;
     fill_normals_kernel<<<(unsigned)((npaths + kBlock - 1) / kBlock), kBlock, 0, s>>>(
-        tables, rc, seed_lo, seed_hi, antithetic, path0, npaths, dim, out);
+        tables, rc, make_philox_keys(seed_lo, seed_hi), antithetic, path0, npaths, dim, out);
     return cudaGetLastError();
 }
 
