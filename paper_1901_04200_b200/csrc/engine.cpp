@@ -722,6 +722,7 @@ HestonArgs heston_args(ltg_ctx* c, const double* x) {
     a.sc.sqdt = a.sqdt;
     a.sc.mu_dt = a.mu_dt;
     a.sc.half_dt = a.half_dt;
+    a.scf = to_float(a.sc);
     a.x = c->x_src;
     a.v0 = x[4];
     if (c->nlev <= (uint32_t)kInlineLev) {
