@@ -407,7 +407,7 @@ def main():
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
                 "basis": ("algorithmic: the kernels' executed " +
                           ("FADD+FMUL+FFMA" if fp32 else "DADD+DMUL+DFMA") +
-                          " per path (ncu census, profiles/r3_census.txt) minus the redundant "
+                          " per path (ncu census, profiles/r4_census.txt) minus the redundant "
                           "AS241 central-branch evaluations on tail slots; pass 2 weighted by "
                           "the draw-store share"),
                 "census_inst_per_path": {b: w[b] for b in w},

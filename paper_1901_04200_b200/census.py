@@ -7,10 +7,12 @@ FMUL + FFMA), one launch divided by its path count. Pass 2 has two rows:
 kept them in the HBM draw store and pass 2 reads them); a call's pass-2
 figure is the two weighted by the fraction of its paths whose draws were
 stored (bench.py reads that from ltg_timing.z_bytes).
-Source: profiles/r3_census.txt (cfg3 at 2^20, cfg1 at 2^16, cfg2 and cfg4 at
+Source: profiles/r4_census.txt (tools/census_from_ncu.py on one
+tools/gpu_profile.sh session; cfg3 at 2^20, cfg1 at 2^16, cfg2 and cfg4 at
 2^18 paths; the round-2 final kernels: S-free pass 2, V-only checkpoints,
 the fp32 mode's single-precision inverse normal, Philox and AS241's central
-branch fused in one loop).
+branch fused in one loop, whole fused iterations stored, step loops in runs
+between maturities).
 
 ALGORITHMIC — EXECUTED minus the kernels' only redundant floating-point work:
 gen_segment evaluates AS241's central branch for every slot of a batch,
@@ -39,22 +41,22 @@ SHAPE = {"cfg1_gbm": (16, 32), "cfg2_localvol": (64, 128), "cfg3_heston": (756, 
 
 # (config, precision) -> {kernel: executed instructions per path}
 EXECUTED: Dict[Tuple[str, str], Dict[str, float]] = {
-    ("cfg3_heston", "fp64"): {"pass1": 104000.6, "pass2_regen": 106463.5, "pass2_store": 30466.4},
-    ("cfg3_heston", "fp32"): {"pass1": 29074.5, "pass2_regen": 42713.0, "pass2_store": 23586.5},
-    ("cfg1_gbm", "fp64"): {"pass1": 2333.5, "pass2_regen": 2418.6, "pass2_store": 814.2},
-    ("cfg1_gbm", "fp32"): {"pass1": 676.7, "pass2_regen": 1001.9, "pass2_store": 597.1},
-    ("cfg2_localvol", "fp64"): {"pass1": 9439.4, "pass2_regen": 11455.2, "pass2_store": 5036.9},
-    ("cfg2_localvol", "fp32"): {"pass1": 2723.1, "pass2_regen": 4536.1, "pass2_store": 2917.1},
+    ("cfg3_heston", "fp64"): {"pass1": 104156.6, "pass2_regen": 105806.5, "pass2_store": 29809.4},
+    ("cfg3_heston", "fp32"): {"pass1": 29074.5, "pass2_regen": 42056.0, "pass2_store": 22929.5},
+    ("cfg1_gbm", "fp64"): {"pass1": 2333.5, "pass2_regen": 2405.6, "pass2_store": 801.2},
+    ("cfg1_gbm", "fp32"): {"pass1": 676.7, "pass2_regen": 988.9, "pass2_store": 584.1},
+    ("cfg2_localvol", "fp64"): {"pass1": 9439.4, "pass2_regen": 11399.2, "pass2_store": 4980.9},
+    ("cfg2_localvol", "fp32"): {"pass1": 2723.1, "pass2_regen": 4480.1, "pass2_store": 2861.1},
     # the basket's pass 2 is a store-mode epilogue (no draws, no replay)
     ("cfg4_basket16", "fp64"): {"pass1": 66348.8, "pass2_regen": 455.1, "pass2_store": 455.1},
 }
 
 # DRAM bytes per path (ncu dram__bytes_read + write), without / with the draw store
 DRAM: Dict[Tuple[str, str], Dict[str, float]] = {
-    ("cfg3_heston", "fp64"): {"pass1": 752.8, "pass1_store": 12849.2, "pass2_regen": 812.9,
-                              "pass2_store": 12914.5},
-    ("cfg3_heston", "fp32"): {"pass1": 352.1, "pass1_store": 6398.9, "pass2_regen": 406.9,
-                              "pass2_store": 6452.9},
+    ("cfg3_heston", "fp64"): {"pass1": 752.8, "pass1_store": 12848.4, "pass2_regen": 811.2,
+                              "pass2_store": 12914.0},
+    ("cfg3_heston", "fp32"): {"pass1": 350.8, "pass1_store": 6399.7, "pass2_regen": 405.0,
+                              "pass2_store": 6452.8},
 }
 
 # central-batch widths and normal batches of the kernels (heston.cu: kPass1PB,
