@@ -427,8 +427,10 @@ def main():
             roof["survey_8d"] = {
                 "W_per_path": w8d,
                 "whole_step_frac": w8d * paths_rank / t_step / peak,
-                "note": "SURVEY.md §8(d) preliminary W (not the census): an upper figure, "
-                        "the bench's frac stays the census"}
+                "note": "SURVEY.md §8(d) preliminary W (not the census): an upper figure — it "
+                        "credits pass 2 with drawing every normal, so it exceeds what the "
+                        "kernels execute wherever pass 2 reads the draw store (and can pass 1.0 "
+                        "when every path's draws are stored); the bench's frac stays the census"}
         trf = census.dram_per_path(cfg.name, prec, dom, zf)
         if trf is not None and args.method == "adjoint":
             # ncu DRAM bytes/path of the dominant kernel (with and without the
