@@ -41,6 +41,8 @@ def test_engine_arm_json_contract():
     r = d["roofline"]
     assert r["bound"] == "fp64" and 0 < r["frac"] < 1.2 and r["peak"] > 1.0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
+    # the census fractions, and SURVEY §8(d)'s W beside them (labelled, not the frac)
+    assert 0 < r["frac"] <= r["executed_frac"] and r["survey_8d"]["W_per_path"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["clocks"]["samples"] >= 0
     assert "tangent" in d["alt_methods"]

@@ -32,3 +32,13 @@ def test_algorithmic_below_executed_and_store_weighting(name, prec):
     assert s < r or name.startswith("cfg4")
     mid = census.per_path(name, prec, "pass2", 0.25)
     assert mid == pytest.approx(0.75 * r + 0.25 * s)
+
+
+def test_survey_w_cross_check_figure():
+    # SURVEY §8(d)'s preliminary W (bench.py roofline.survey_8d): an upper
+    # figure beside the census, never below the executed count of both passes
+    assert census.survey_w("cfg5_heston_scaling") == census.survey_w("cfg3_heston") == 2.6e5
+    for name in ("cfg1_gbm", "cfg2_localvol", "cfg3_heston", "cfg4_basket16"):
+        both = sum(census.per_path(name, "fp64", k, 0.0, "executed") for k in ("pass1", "pass2"))
+        assert census.survey_w(name) >= both * 0.45  # the same order of magnitude
+    assert census.survey_w("no_such_config") is None
