@@ -46,17 +46,17 @@ EXECUTED: Dict[Tuple[str, str], Dict[str, float]] = {
     ("cfg1_gbm", "fp64"): {"pass1": 2333.5, "pass2_regen": 2405.6, "pass2_store": 801.2},
     ("cfg1_gbm", "fp32"): {"pass1": 676.7, "pass2_regen": 988.9, "pass2_store": 584.1},
     ("cfg2_localvol", "fp64"): {"pass1": 9439.4, "pass2_regen": 11399.2, "pass2_store": 4980.9},
-    ("cfg2_localvol", "fp32"): {"pass1": 2723.1, "pass2_regen": 4480.1, "pass2_store": 2861.1},
+    ("cfg2_localvol", "fp32"): {"pass1": 2723.1, "pass2_regen": 4496.1, "pass2_store": 2861.1},
     # the basket's pass 2 is a store-mode epilogue (no draws, no replay)
     ("cfg4_basket16", "fp64"): {"pass1": 66348.8, "pass2_regen": 455.1, "pass2_store": 455.1},
 }
 
 # DRAM bytes per path (ncu dram__bytes_read + write), without / with the draw store
 DRAM: Dict[Tuple[str, str], Dict[str, float]] = {
-    ("cfg3_heston", "fp64"): {"pass1": 752.8, "pass1_store": 12848.4, "pass2_regen": 811.2,
-                              "pass2_store": 12914.0},
-    ("cfg3_heston", "fp32"): {"pass1": 350.8, "pass1_store": 6399.7, "pass2_regen": 405.0,
-                              "pass2_store": 6452.8},
+    ("cfg3_heston", "fp64"): {"pass1": 751.8, "pass1_store": 12850.9, "pass2_regen": 810.0,
+                              "pass2_store": 12911.0},
+    ("cfg3_heston", "fp32"): {"pass1": 351.4, "pass1_store": 6400.0, "pass2_regen": 405.1,
+                              "pass2_store": 6452.7},
 }
 
 # central-batch widths and normal batches of the kernels (heston.cu: kPass1PB,
