@@ -22,9 +22,9 @@ for (name, prec), d in census.DRAM.items():
     print(f"{name:16s} {prec:5s} " + "  ".join(f"{k} {v:.1f}" for k, v in d.items()))
 print("""
 # kernel times at 2^20 paths (ncu gpu__time_duration, serialised, cold):
-#   fp64 pass 1  9.68 ms (z0) /  9.94 ms (z1, writes the draw store); pass 2 10.18 ms (z0) / 3.57 ms (z1)
+#   fp64 pass 1  9.68 ms (z0) /  9.93 ms (z1, writes the draw store); pass 2  9.91 ms (z0) / 3.80 ms (z1)
 #   fp32 pass 1  4.33 ms (z0) /  4.54 ms (z1);                        pass 2  4.96 ms (z0) / 2.15 ms (z1)
-# pipe use (cfg3 fp64, z0): pass 1 FP64 pipe 64.8%, issue 64.7%; pass 2 FP64 pipe 62.5%, issue 62.9%
-#            (fp32, z0):   pass 1 issue 75.7%; pass 2 issue 77.0%
-# warp instructions per path-step (fp64, z0): pass 1 289 (r3: 308, r2: 324), pass 2 295 (r3: 315, r2: 339);
+# pipe use (cfg3 fp64, z0): pass 1 FP64 pipe 64.8%, issue 64.7%; pass 2 FP64 pipe 64.0%, issue 65.6%
+#            (fp32, z0):   pass 1 issue 75.7%; pass 2 issue 77.3%
+# warp instructions per path-step (fp64, z0): pass 1 289 (r3: 308, r2: 324), pass 2 300 (r3: 315, r2: 339);
 #            (fp32, z0):   pass 1 151 (r3: 175), pass 2 177 (r3: 200)""")
